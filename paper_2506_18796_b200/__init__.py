@@ -1,0 +1,35 @@
+"""B200-native trace-replay engine for CACE (Context-Aware CodeLLM Eviction, arXiv 2506.18796).
+
+The hot path — replaying request traces under the CACE / LRU / ablation
+eviction policies for many independent scenarios — runs as hand-written
+sm_100a CUDA kernels behind the C ABI in ``include/cace_gpu.h``
+(``lib/libcace_gpu.so``).  This package is the Python mirror of the reference
+simulator's API over that ABI (``api``), the synthetic workload builders of
+BASELINE.json's configs (``synth``) and the multi-GPU scenario sharding
+(``shard``).  Importing it loads the CUDA library and fails loudly if it is
+missing; there is no CPU fallback.
+"""
+from .api import (  # noqa: F401
+    ClusterConfig,
+    Engine,
+    Language,
+    ModelCatalog,
+    ModelDescriptor,
+    P1Mode,
+    PolicyConfig,
+    SimError,
+    SimulationReport,
+    TaskClass,
+    Trace,
+    Variant,
+    dedup_window,
+    device_count,
+    eviction_score,
+    make_scenarios,
+    run,
+    run_batch,
+    select_victim,
+    service_times,
+    version,
+)
+from ._native import SCENARIO_DTYPE, SUMMARY_DTYPE  # noqa: F401

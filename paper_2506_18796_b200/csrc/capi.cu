@@ -1,0 +1,798 @@
+// C-ABI implementation of include/cace_gpu.h: host-side validation, trace
+// layout, scenario planning and kernel launches.  There is no CPU fallback:
+// without a CUDA device every replay entry returns CACE_E_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cace_gpu.h"
+#include "glibc_log.cuh"
+#include "policy_kernels.cuh"
+#include "replay_lane.cuh"
+
+using namespace cace;
+
+namespace {
+
+const double kLogTab[256] = CACE_GLIBC_LOG_TAB;
+const double kLogTab2[256] = CACE_GLIBC_LOG_TAB2;
+
+void put_msg(char* msg, size_t cap, const std::string& s) {
+  if (!msg || cap == 0) return;
+  const size_t k = std::min(cap - 1, s.size());
+  std::memcpy(msg, s.data(), k);
+  msg[k] = 0;
+}
+
+struct CudaFail {
+  int32_t code;
+  std::string what;
+};
+
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess)                                                        \
+      throw CudaFail{CACE_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+struct Invalid {
+  int32_t code;
+  std::string what;
+};
+
+// Device buffer owned by RAII.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t k) {
+    release();
+    n = k;
+    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
+  }
+  void upload(const T* h, size_t k, cudaStream_t s) {
+    alloc(k);
+    if (k) CK(cudaMemcpyAsync(p, h, k * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+int g_probe = -2;
+std::mutex g_probe_mu;
+
+int probe_log_variant() {
+  std::lock_guard<std::mutex> lk(g_probe_mu);
+  if (g_probe != -2) return g_probe;
+  // Deterministic inputs covering both paths: near 1 and log-uniform wide.
+  bool ok_fma = true, ok_sse = true;
+  uint64_t st = 0x9e3779b97f4a7c15ULL;
+  for (int i = 0; i < (1 << 20) && (ok_fma || ok_sse); ++i) {
+    st += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = st;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    const double x = (i & 1) ? 1.0 + u * 0.0647 : std::exp2(u * 40.0);
+    const double ref = std::log(x);
+    const double a = cace_glibc_log(x, CACE_LOG_FMA, kLogTab, kLogTab2);
+    const double b = cace_glibc_log(x, CACE_LOG_SSE2, kLogTab, kLogTab2);
+    uint64_t ur, ua, ub;
+    std::memcpy(&ur, &ref, 8);
+    std::memcpy(&ua, &a, 8);
+    std::memcpy(&ub, &b, 8);
+    ok_fma = ok_fma && ur == ua;
+    ok_sse = ok_sse && ur == ub;
+  }
+  g_probe = ok_fma ? CACE_LOG_FMA : (ok_sse ? CACE_LOG_SSE2 : -1);
+  return g_probe;
+}
+
+int resolve_log_variant(const cace_opts_t* o) {
+  if (o && o->log_variant >= 0) return o->log_variant;
+  const int v = probe_log_variant();
+  return v < 0 ? CACE_LOG_FMA : v;
+}
+
+int32_t device_count() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void require_device(const cace_opts_t* o) {
+  const int n = device_count();
+  if (n <= 0) throw Invalid{CACE_E_NO_DEVICE, "cace: no CUDA device (there is no CPU fallback)"};
+  const int dev = o ? o->device : 0;
+  if (dev < 0 || dev >= n) throw Invalid{CACE_E_INVALID, "cace: device ordinal out of range"};
+  CK(cudaSetDevice(dev));
+}
+
+std::string model_name(const std::vector<std::string>& ids, int m) {
+  if (m >= 0 && m < (int)ids.size() && !ids[m].empty()) return ids[m];
+  return "model#" + std::to_string(m);
+}
+
+// Host copy of the catalog + device columns.
+struct Catalog {
+  int M = 0;
+  std::vector<double> lt, pr, dr, tok, p2;
+  std::vector<int32_t> lex, cls;
+  std::vector<std::string> ids;
+  DBuf<double> d_lt, d_p2, d_tok;
+  DBuf<int32_t> d_lex;
+
+  void load(const cace_catalog_t* c) {
+    if (!c || c->n_models < 1 || c->n_models > 65535 || !c->load_time_s || !c->prefill_rate_tps ||
+        !c->decode_rate_tps || !c->expected_output_tokens || !c->lex_rank || !c->task_class)
+      throw Invalid{CACE_E_INVALID, "cace: malformed catalog"};
+    M = c->n_models;
+    lt.assign(c->load_time_s, c->load_time_s + M);
+    pr.assign(c->prefill_rate_tps, c->prefill_rate_tps + M);
+    dr.assign(c->decode_rate_tps, c->decode_rate_tps + M);
+    tok.resize(M);
+    p2.resize(M);
+    for (int m = 0; m < M; ++m) {
+      tok[m] = (double)c->expected_output_tokens[m];
+      p2[m] = 1.0 / (1.0 + lt[m] / 100.0);  // policy.cpp:55
+    }
+    lex.assign(c->lex_rank, c->lex_rank + M);
+    cls.assign(c->task_class, c->task_class + M);
+    ids.assign(M, std::string());
+    if (c->model_id)
+      for (int m = 0; m < M; ++m)
+        if (c->model_id[m]) ids[m] = c->model_id[m];
+  }
+  void upload(cudaStream_t s) {
+    d_lt.upload(lt.data(), M, s);
+    d_p2.upload(p2.data(), M, s);
+    d_tok.upload(tok.data(), M, s);
+    d_lex.upload(lex.data(), M, s);
+  }
+  DevCatalog dev() const { return DevCatalog{M, d_lt.p, d_p2.p, d_tok.p, d_lex.p}; }
+  bool bad_rates(int m) const { return pr[m] <= 0 || dr[m] <= 0; }  // engine.cpp:17
+};
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+struct cace_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int log_variant = CACE_LOG_FMA;
+  Catalog cat;
+  int T = 0;
+  std::vector<int64_t> off;        // [T+1]
+  std::vector<int32_t> bad_model;  // [T] first (sorted) request model with bad rates, or -1
+  DBuf<ReqRec> d_rec;
+  DBuf<int64_t> d_off;
+  DBuf<uint32_t> d_first0, d_perm;
+  DBuf<double> d_tab, d_tab2;
+  // plan
+  int64_t plan_n = -1;
+  struct Seg {
+    int C;
+    int64_t b, e;
+  };
+  std::vector<Seg> segs;
+  DBuf<int64_t> d_order;
+  std::vector<int64_t> bad_idx;
+  std::vector<int32_t> bad_code;
+  DBuf<int64_t> d_bad_idx;
+  DBuf<int32_t> d_bad_code;
+  int last_launches = 0;
+};
+
+namespace {
+
+constexpr int kMaxLaneC = 16;
+
+void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trace_t* traces,
+                  int32_t n_traces, const cace_opts_t* opts) {
+  require_device(opts);
+  e->device = opts ? opts->device : 0;
+  if (opts && opts->stream) {
+    e->stream = static_cast<cudaStream_t>(opts->stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->own_stream = true;
+  }
+  e->log_variant = resolve_log_variant(opts);
+  e->cat.load(catalog);
+  const int M = e->cat.M;
+  if (n_traces < 0 || (n_traces > 0 && !traces)) throw Invalid{CACE_E_INVALID, "cace: bad traces"};
+  e->T = n_traces;
+  e->off.assign(n_traces + 1, 0);
+  for (int t = 0; t < n_traces; ++t) {
+    if (traces[t].n_requests < 0 || traces[t].n_requests > 0xfffffff0LL)
+      throw Invalid{CACE_E_INVALID, "cace: trace too long"};
+    e->off[t + 1] = e->off[t] + traces[t].n_requests;
+  }
+  const int64_t N = e->off[n_traces];
+  std::vector<ReqRec> rec(N);
+  std::vector<uint32_t> perm(N), first0((size_t)n_traces * M);
+  e->bad_model.assign(n_traces, -1);
+  std::vector<uint32_t> last(M);
+  for (int t = 0; t < n_traces; ++t) {
+    const cace_trace_t& tr = traces[t];
+    const int64_t n = tr.n_requests, b = e->off[t];
+    if (n > 0 && (!tr.arrival_time_s || !tr.model || !tr.prompt_tokens || !tr.output_tokens))
+      throw Invalid{CACE_E_INVALID, "cace: trace arrays missing"};
+    // run() resolves every request's model first (engine.cpp:87-92).
+    for (int64_t i = 0; i < n; ++i) {
+      const int m = tr.model[i];
+      if (m < 0 || m >= M)
+        throw Invalid{CACE_E_LOOKUP, "catalog: no model registered for model index " +
+                                         std::to_string(m)};
+      if (!std::isfinite(tr.arrival_time_s[i]))
+        throw Invalid{CACE_E_INVALID, "cace: non-finite arrival_time_s"};
+    }
+    // Replay order = Arrival pop order (time, seq=index) (engine.cpp:49-55).
+    std::vector<uint32_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0u);
+    bool sorted = true;
+    for (int64_t i = 1; i < n && sorted; ++i)
+      sorted = !(tr.arrival_time_s[i] < tr.arrival_time_s[i - 1]);
+    if (!sorted)
+      std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
+        return tr.arrival_time_s[x] < tr.arrival_time_s[y];
+      });
+    for (int m = 0; m < M; ++m) last[m] = (uint32_t)n;
+    for (int64_t k = n - 1; k >= 0; --k) {
+      const uint32_t i = ord[k];
+      const int m = tr.model[i];
+      ReqRec& r = rec[b + k];
+      r.arrival = tr.arrival_time_s[i];
+      // service_times (engine.cpp:15-26)
+      r.prefill = (double)tr.prompt_tokens[i] / e->cat.pr[m];
+      r.decode = (double)std::max(tr.output_tokens[i], 1) / e->cat.dr[m];
+      r.nxt = last[m];
+      r.mc = (uint32_t)m | ((uint32_t)(e->cat.cls[m] == CACE_REASONING) << 16);
+      last[m] = (uint32_t)k;
+      perm[b + k] = i;
+      if (e->cat.bad_rates(m)) e->bad_model[t] = m;  // ends as the first in replay order
+    }
+    for (int m = 0; m < M; ++m) first0[(size_t)t * M + m] = last[m];
+  }
+  cudaStream_t s = e->stream;
+  e->cat.upload(s);
+  e->d_rec.upload(rec.data(), N, s);
+  e->d_off.upload(e->off.data(), e->off.size(), s);
+  e->d_first0.upload(first0.data(), first0.size(), s);
+  e->d_perm.upload(perm.data(), perm.size(), s);
+  e->d_tab.upload(kLogTab, 256, s);
+  e->d_tab2.upload(kLogTab2, 256, s);
+  CK(cudaStreamSynchronize(s));
+}
+
+// Reference run() preconditions (engine.cpp:79-92, 17-20) per scenario.
+int32_t precheck(const cace_engine* e, const cace_scenario_t& sc) {
+  if (sc.trace < 0 || sc.trace >= e->T) return CACE_E_INVALID;
+  if (sc.variant < CACE_LRU || sc.variant > CACE_MINUS_P4) return CACE_E_INVALID;
+  if (sc.window_length < 1) return CACE_E_WINDOW;
+  if (sc.num_accelerators < 1) return CACE_E_ACCELERATORS;
+  const int64_t n = e->off[sc.trace + 1] - e->off[sc.trace];
+  if (n == 0) return CACE_OK;
+  if (e->bad_model[sc.trace] >= 0) return CACE_E_RATES | (e->bad_model[sc.trace] << 8);
+  const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
+  if (cap < 1) return CACE_E_DEADLOCK;  // nothing can ever load (engine.cpp:235-237)
+  if (cap > kMaxLaneC) return CACE_E_INVALID;
+  return CACE_OK;
+}
+
+void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
+  if (n < 0 || (n > 0 && !sc)) throw Invalid{CACE_E_INVALID, "cace: bad scenario array"};
+  e->segs.clear();
+  e->bad_idx.clear();
+  e->bad_code.clear();
+  std::vector<int64_t> ok;
+  ok.reserve(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t st = precheck(e, sc[i]);
+    const int64_t len = e->off[sc[i].trace >= 0 && sc[i].trace < e->T ? sc[i].trace + 1 : 0] -
+                        e->off[sc[i].trace >= 0 && sc[i].trace < e->T ? sc[i].trace : 0];
+    if (st != CACE_OK || len == 0) {
+      e->bad_idx.push_back(i);
+      e->bad_code.push_back(st);
+    } else {
+      ok.push_back(i);
+    }
+  }
+  auto capof = [&](int64_t i) {
+    return (int)((int64_t)sc[i].num_accelerators * sc[i].models_per_accelerator);
+  };
+  // Coherent warps: capacity (template), then trace, then the control-flow
+  // shaping policy fields.
+  std::stable_sort(ok.begin(), ok.end(), [&](int64_t a, int64_t b) {
+    const cace_scenario_t &x = sc[a], &y = sc[b];
+    const int ca = capof(a), cb = capof(b);
+    if (ca != cb) return ca < cb;
+    if (x.trace != y.trace) return x.trace < y.trace;
+    if (x.variant != y.variant) return x.variant < y.variant;
+    if (x.window_length != y.window_length) return x.window_length < y.window_length;
+    return x.p1_mode < y.p1_mode;
+  });
+  for (size_t k = 0; k < ok.size();) {
+    const int C = capof(ok[k]);
+    size_t j = k;
+    while (j < ok.size() && capof(ok[j]) == C) ++j;
+    e->segs.push_back({C, (int64_t)k, (int64_t)j});
+    k = j;
+  }
+  e->d_order.upload(ok.data(), ok.size(), e->stream);
+  e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
+  e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);
+  CK(cudaStreamSynchronize(e->stream));
+  e->plan_n = n;
+}
+
+template <int C>
+void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+  static bool attr_set = false;  // per-process; smem need is bounded by M
+  if (smem > 48 * 1024 && !attr_set) {
+    CK(cudaFuncSetAttribute(replay_lane_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            227 * 1024));
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
+  replay_lane_kernel<C><<<grid, LANE_BLOCK, smem, s>>>(P);
+  CK(cudaGetLastError());
+}
+
+void dispatch_lane(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+  switch (C) {
+#define CASE(k) \
+  case k: launch_lane<k>(P, count, smem, s); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: throw Invalid{CACE_E_INVALID, "cace: capacity not supported by the lane kernel"};
+  }
+}
+
+void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary_t* d_out,
+            const DumpDev& dump, cudaStream_t s) {
+  if (n != e->plan_n) throw Invalid{CACE_E_INVALID, "cace: replay does not match the plan"};
+  CK(cudaSetDevice(e->device));
+  ReplayParams P{};
+  P.rec = e->d_rec.p;
+  P.trace_off = e->d_off.p;
+  P.first0 = e->d_first0.p;
+  P.perm = e->d_perm.p;
+  P.cat = e->cat.dev();
+  P.log_tab = e->d_tab.p;
+  P.log_tab2 = e->d_tab2.p;
+  P.log_variant = e->log_variant;
+  P.scen = d_sc;
+  P.order = e->d_order.p;
+  P.out = d_out;
+  P.dump = dump;
+  const size_t smem = lane_smem_bytes(e->cat.M);
+  e->last_launches = 0;
+  for (const auto& g : e->segs) {
+    P.seg_begin = g.b;
+    P.seg_end = g.e;
+    dispatch_lane(g.C, P, g.e - g.b, smem, s);
+    ++e->last_launches;
+  }
+  if (!e->bad_idx.empty()) {
+    fill_status_kernel<<<(unsigned)((e->bad_idx.size() + 255) / 256), 256, 0, s>>>(
+        e->d_bad_idx.p, e->d_bad_code.p, (int64_t)e->bad_idx.size(), d_out);
+    CK(cudaGetLastError());
+    ++e->last_launches;
+  }
+}
+
+std::string status_text(const cace_engine* e, int32_t status) {
+  const int code = status & 0xff;
+  const int m = status >> 8;
+  switch (code) {
+    case CACE_OK: return "";
+    case CACE_E_WINDOW: return "run: window_length must be >= 1";
+    case CACE_E_ACCELERATORS: return "run: need at least one accelerator";
+    case CACE_E_RATES: return "service_times: rates must be positive for " + model_name(e->cat.ids, m);
+    case CACE_E_CLOCK:
+      return "eviction_score: clock precedes last_used_s for " + model_name(e->cat.ids, m);
+    case CACE_E_DEADLOCK: return "run: deadlock \xe2\x80\x94 pending requests with no schedulable event";
+    case CACE_E_RESIDENCY: return "run: residency bound violated";
+    default: return "cace: invalid scenario (bad trace index, variant, or capacity > 16)";
+  }
+}
+
+template <typename F>
+int32_t guarded(char* msg, size_t cap, F&& f) {
+  try {
+    return f();
+  } catch (const CudaFail& x) {
+    put_msg(msg, cap, x.what);
+    return x.code;
+  } catch (const Invalid& x) {
+    put_msg(msg, cap, x.what);
+    return x.code;
+  } catch (const std::exception& x) {
+    put_msg(msg, cap, x.what());
+    return CACE_E_INVALID;
+  }
+}
+
+}  // namespace
+
+// ==========================================================================
+extern "C" {
+
+const char* cace_version(void) {
+  return "cace-b200 0.1 (sm_100a lane-per-scenario replay; glibc-log bit-exact P1)";
+}
+int32_t cace_abi_version(void) { return CACE_ABI_VERSION; }
+int32_t cace_device_count(void) { return device_count(); }
+
+int32_t cace_engine_create(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                           int32_t n_traces, const cace_opts_t* opts, cace_engine** out,
+                           char* msg, size_t msg_cap) {
+  if (!out) return CACE_E_INVALID;
+  *out = nullptr;
+  cace_engine* e = new cace_engine();
+  const int32_t rc = guarded(msg, msg_cap, [&]() -> int32_t {
+    build_engine(e, catalog, traces, n_traces, opts);
+    return CACE_OK;
+  });
+  if (rc != CACE_OK) {
+    cace_engine_destroy(e);
+    return rc;
+  }
+  *out = e;
+  return CACE_OK;
+}
+
+void cace_engine_destroy(cace_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+int32_t cace_engine_plan(cace_engine* e, const cace_scenario_t* scenarios, int64_t n, char* msg,
+                         size_t msg_cap) {
+  if (!e) return CACE_E_INVALID;
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    CK(cudaSetDevice(e->device));
+    plan(e, scenarios, n);
+    return CACE_OK;
+  });
+}
+
+int32_t cace_engine_replay_device(cace_engine* e, const cace_scenario_t* d_scenarios, int64_t n,
+                                  cace_summary_t* d_summaries, void* stream, char* msg,
+                                  size_t msg_cap) {
+  if (!e) return CACE_E_INVALID;
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    replay(e, d_scenarios, n, d_summaries, DumpDev{},
+           stream ? static_cast<cudaStream_t>(stream) : e->stream);
+    return CACE_OK;
+  });
+}
+
+int32_t cace_engine_status_message(const cace_engine* e, int32_t status, char* msg,
+                                   size_t msg_cap) {
+  if (!e) return CACE_E_INVALID;
+  put_msg(msg, msg_cap, status_text(e, status));
+  return status & 0xff;
+}
+
+int32_t cace_engine_last_launches(const cace_engine* e) { return e ? e->last_launches : 0; }
+
+int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                          int32_t n_traces, const cace_scenario_t* scenarios, int64_t n_scenarios,
+                          cace_summary_t* summaries, const cace_dump_t* dump,
+                          const cace_opts_t* opts, char* msg, size_t msg_cap) {
+  cace_engine* e = nullptr;
+  int32_t rc = cace_engine_create(catalog, traces, n_traces, opts, &e, msg, msg_cap);
+  if (rc != CACE_OK) return rc;
+  rc = guarded(msg, msg_cap, [&]() -> int32_t {
+    if (n_scenarios > 0 && !summaries) throw Invalid{CACE_E_INVALID, "cace: summaries is NULL"};
+    plan(e, scenarios, n_scenarios);
+    cudaStream_t s = e->stream;
+    DBuf<cace_scenario_t> d_sc;
+    d_sc.upload(scenarios, n_scenarios, s);
+    DBuf<cace_summary_t> d_out;
+    d_out.alloc(n_scenarios);
+    // Optional full dump.
+    DumpDev dd{};
+    DBuf<int32_t> d_slot;
+    DBuf<int64_t> d_doff, d_nev;
+    DBuf<uint8_t> d_cold;
+    DBuf<double> d_qw, d_lw, d_pf, d_dc, d_tt, d_ee, d_ec;
+    DBuf<int32_t> d_em;
+    std::vector<int64_t> doff;
+    int64_t total = 0;
+    const int nd = dump ? dump->n_dump : 0;
+    if (nd > 0) {
+      std::vector<int32_t> slot(n_scenarios, -1);
+      for (int k = 0; k < nd; ++k) {
+        const int64_t si = dump->scenario_index[k];
+        if (si < 0 || si >= n_scenarios) throw Invalid{CACE_E_INVALID, "cace: bad dump index"};
+        slot[si] = k;
+        doff.push_back(total);
+        const int t = scenarios[si].trace;
+        total += (t >= 0 && t < e->T) ? e->off[t + 1] - e->off[t] : 0;
+      }
+      d_slot.upload(slot.data(), slot.size(), s);
+      d_doff.upload(doff.data(), doff.size(), s);
+      dd.slot = d_slot.p;
+      dd.dump_off = d_doff.p;
+      auto mk = [&](DBuf<double>& b, double* h) -> double* {
+        if (!h) return nullptr;
+        b.alloc(total);
+        return b.p;
+      };
+      if (dump->cold_start) {
+        d_cold.alloc(total);
+        dd.cold = d_cold.p;
+      }
+      dd.queue_wait = mk(d_qw, dump->queue_wait_s);
+      dd.load_wait = mk(d_lw, dump->load_wait_s);
+      dd.prefill = mk(d_pf, dump->prefill_s);
+      dd.decode = mk(d_dc, dump->decode_s);
+      dd.ttft = mk(d_tt, dump->ttft_s);
+      dd.e2e = mk(d_ee, dump->e2e_s);
+      dd.evict_cap = dump->evict_cap;
+      if (dump->evict_model && dump->evict_cap > 0) {
+        d_em.alloc((size_t)nd * dump->evict_cap);
+        dd.evict_model = d_em.p;
+      }
+      if (dump->evict_clock && dump->evict_cap > 0) {
+        d_ec.alloc((size_t)nd * dump->evict_cap);
+        dd.evict_clock = d_ec.p;
+      }
+      d_nev.alloc(nd);
+      CK(cudaMemsetAsync(d_nev.p, 0, nd * sizeof(int64_t), s));
+      dd.n_evict = d_nev.p;
+    }
+    replay(e, d_sc.p, n_scenarios, d_out.p, dd, s);
+    if (n_scenarios > 0)
+      CK(cudaMemcpyAsync(summaries, d_out.p, n_scenarios * sizeof(cace_summary_t),
+                         cudaMemcpyDeviceToHost, s));
+    if (nd > 0) {
+      auto back = [&](void* h, const void* d, size_t bytes) {
+        if (h && d && bytes) CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+      };
+      back(dump->cold_start, d_cold.p, total);
+      back(dump->queue_wait_s, d_qw.p, total * 8);
+      back(dump->load_wait_s, d_lw.p, total * 8);
+      back(dump->prefill_s, d_pf.p, total * 8);
+      back(dump->decode_s, d_dc.p, total * 8);
+      back(dump->ttft_s, d_tt.p, total * 8);
+      back(dump->e2e_s, d_ee.p, total * 8);
+      back(dump->evict_model, d_em.p, (size_t)nd * dump->evict_cap * 4);
+      back(dump->evict_clock, d_ec.p, (size_t)nd * dump->evict_cap * 8);
+      back(dump->n_evict, d_nev.p, (size_t)nd * 8);
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n_scenarios; ++i) {
+      if (summaries[i].status != CACE_OK) {
+        put_msg(msg, msg_cap, status_text(e, summaries[i].status));
+        return summaries[i].status & 0xff;
+      }
+    }
+    return CACE_OK;
+  });
+  cace_engine_destroy(e);
+  return rc;
+}
+
+// ---------------- policy-level batch entry points ------------------------
+
+int32_t cace_select_victim_batch(const cace_catalog_t* catalog, int64_t n_instances,
+                                 int32_t max_entries, const int32_t* n_entries,
+                                 const int32_t* entry_model, const double* entry_last_used,
+                                 const uint8_t* entry_busy, int32_t max_window,
+                                 const int32_t* n_window, const int32_t* window_models,
+                                 const double* clock, const cace_scenario_t* policy,
+                                 int32_t* victim_out, const cace_opts_t* opts, char* msg,
+                                 size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    Catalog cat;
+    cat.load(catalog);
+    if (n_instances <= 0) return CACE_OK;
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    cat.upload(s);
+    const size_t NE = (size_t)n_instances * max_entries, NW = (size_t)n_instances * max_window;
+    DBuf<int32_t> d_ne, d_em, d_nw, d_wm, d_v, d_st;
+    DBuf<double> d_lu, d_clk, d_tab, d_tab2;
+    DBuf<uint8_t> d_busy;
+    DBuf<cace_scenario_t> d_pol;
+    d_ne.upload(n_entries, n_instances, s);
+    d_em.upload(entry_model, NE, s);
+    d_lu.upload(entry_last_used, NE, s);
+    d_busy.upload(entry_busy, NE, s);
+    d_nw.upload(n_window, n_instances, s);
+    if (NW) d_wm.upload(window_models, NW, s);
+    d_clk.upload(clock, n_instances, s);
+    d_pol.upload(policy, n_instances, s);
+    d_tab.upload(kLogTab, 256, s);
+    d_tab2.upload(kLogTab2, 256, s);
+    d_v.alloc(n_instances);
+    d_st.alloc(n_instances);
+    select_victim_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
+        cat.dev(), n_instances, max_entries, d_ne.p, d_em.p, d_lu.p, d_busy.p, max_window, d_nw.p,
+        d_wm.p, d_clk.p, d_pol.p, d_tab.p, d_tab2.p, resolve_log_variant(opts), d_v.p, d_st.p);
+    CK(cudaGetLastError());
+    std::vector<int32_t> st(n_instances);
+    CK(cudaMemcpyAsync(victim_out, d_v.p, n_instances * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(st.data(), d_st.p, n_instances * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int64_t b = 0; b < n_instances; ++b)
+      if (st[b] != CACE_OK) {
+        const int m = st[b] >> 8;
+        put_msg(msg, msg_cap,
+                (st[b] & 0xff) == CACE_E_CLOCK
+                    ? "eviction_score: clock precedes last_used_s for " + model_name(cat.ids, m)
+                    : "catalog: unknown model_id " + model_name(cat.ids, m));
+        return st[b] & 0xff;
+      }
+    return CACE_OK;
+  });
+}
+
+int32_t cace_eviction_score_batch(const cace_catalog_t* catalog, int64_t n_instances,
+                                  const int32_t* model, const double* last_used,
+                                  int32_t max_window, const int32_t* n_window,
+                                  const int32_t* window_models, const double* clock,
+                                  const cace_scenario_t* policy, double* out,
+                                  const cace_opts_t* opts, char* msg, size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    Catalog cat;
+    cat.load(catalog);
+    if (n_instances <= 0) return CACE_OK;
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    cat.upload(s);
+    const size_t NW = (size_t)n_instances * max_window;
+    DBuf<int32_t> d_m, d_nw, d_wm, d_st;
+    DBuf<double> d_lu, d_clk, d_out, d_tab, d_tab2;
+    DBuf<cace_scenario_t> d_pol;
+    d_m.upload(model, n_instances, s);
+    d_lu.upload(last_used, n_instances, s);
+    d_nw.upload(n_window, n_instances, s);
+    if (NW) d_wm.upload(window_models, NW, s);
+    d_clk.upload(clock, n_instances, s);
+    d_pol.upload(policy, n_instances, s);
+    d_tab.upload(kLogTab, 256, s);
+    d_tab2.upload(kLogTab2, 256, s);
+    d_out.alloc((size_t)n_instances * 5);
+    d_st.alloc(n_instances);
+    eviction_score_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
+        cat.dev(), n_instances, d_m.p, d_lu.p, max_window, d_nw.p, d_wm.p, d_clk.p, d_pol.p,
+        d_tab.p, d_tab2.p, resolve_log_variant(opts), d_out.p, d_st.p);
+    CK(cudaGetLastError());
+    std::vector<int32_t> st(n_instances);
+    CK(cudaMemcpyAsync(out, d_out.p, (size_t)n_instances * 5 * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(st.data(), d_st.p, n_instances * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int64_t b = 0; b < n_instances; ++b)
+      if (st[b] != CACE_OK) {
+        put_msg(msg, msg_cap,
+                "eviction_score: clock precedes last_used_s for " + model_name(cat.ids, model[b]));
+        return CACE_E_CLOCK;
+      }
+    return CACE_OK;
+  });
+}
+
+int32_t cace_dedup_window_batch(int64_t n_instances, int32_t max_pending, const int32_t* n_pending,
+                                const int32_t* pending_models, const int32_t* length,
+                                int32_t* out_models, int32_t* n_out, const cace_opts_t* opts,
+                                char* msg, size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    for (int64_t b = 0; b < n_instances; ++b)
+      if (length[b] < 1) {  // policy.cpp:23
+        put_msg(msg, msg_cap, "dedup_window: length must be >= 1");
+        return CACE_E_DEDUP_LENGTH;
+      }
+    if (n_instances <= 0) return CACE_OK;
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    const size_t NP = (size_t)n_instances * max_pending;
+    DBuf<int32_t> d_np, d_pm, d_len, d_om, d_no;
+    d_np.upload(n_pending, n_instances, s);
+    if (NP) d_pm.upload(pending_models, NP, s);
+    d_len.upload(length, n_instances, s);
+    d_om.alloc(NP ? NP : 1);
+    d_no.alloc(n_instances);
+    dedup_window_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
+        n_instances, max_pending, d_np.p, d_pm.p, d_len.p, d_om.p, d_no.p);
+    CK(cudaGetLastError());
+    if (NP) CK(cudaMemcpyAsync(out_models, d_om.p, NP * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(n_out, d_no.p, n_instances * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CACE_OK;
+  });
+}
+
+int32_t cace_service_times_batch(const cace_catalog_t* catalog, int64_t n, const int32_t* model,
+                                 const int32_t* prompt_tokens, const int32_t* output_tokens,
+                                 double* prefill_s, double* decode_s, const cace_opts_t* opts,
+                                 char* msg, size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    Catalog cat;
+    cat.load(catalog);
+    for (int64_t i = 0; i < n; ++i) {
+      const int m = model[i];
+      if (m < 0 || m >= cat.M) throw Invalid{CACE_E_LOOKUP, "catalog: unknown model index"};
+      if (cat.bad_rates(m)) {  // engine.cpp:17-20
+        put_msg(msg, msg_cap, "service_times: rates must be positive for " + model_name(cat.ids, m));
+        return CACE_E_RATES;
+      }
+    }
+    if (n <= 0) return CACE_OK;
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    DBuf<double> d_pr, d_dr, d_pf, d_dc;
+    DBuf<int32_t> d_m, d_p, d_o;
+    d_pr.upload(cat.pr.data(), cat.M, s);
+    d_dr.upload(cat.dr.data(), cat.M, s);
+    d_m.upload(model, n, s);
+    d_p.upload(prompt_tokens, n, s);
+    d_o.upload(output_tokens, n, s);
+    d_pf.alloc(n);
+    d_dc.alloc(n);
+    service_times_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, d_m.p, d_p.p, d_o.p, d_pr.p,
+                                                                      d_dr.p, d_pf.p, d_dc.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(prefill_s, d_pf.p, n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(decode_s, d_dc.p, n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CACE_OK;
+  });
+}
+
+int32_t cace_log_selftest(const double* x, int64_t n, int32_t log_variant, double* out,
+                          const cace_opts_t* opts, char* msg, size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    if (n <= 0) return CACE_OK;
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    const int v = log_variant >= 0 ? log_variant : resolve_log_variant(opts);
+    DBuf<double> d_x, d_o, d_tab, d_tab2;
+    d_x.upload(x, n, s);
+    d_o.alloc(n);
+    d_tab.upload(kLogTab, 256, s);
+    d_tab2.upload(kLogTab2, 256, s);
+    log_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, d_x.p, v, d_tab.p, d_tab2.p, d_o.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d_o.p, n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CACE_OK;
+  });
+}
+
+void cace_log_host(const double* x, int64_t n, int32_t log_variant, double* out) {
+  const int v = log_variant >= 0 ? log_variant : resolve_log_variant(nullptr);
+  for (int64_t i = 0; i < n; ++i) out[i] = cace_glibc_log(x[i], v, kLogTab, kLogTab2);
+}
+
+int32_t cace_probe_log_variant(void) { return probe_log_variant(); }
+
+}  // extern "C"

@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA replay engine vs the compiled reference simulator.
+
+Bar (BASELINE.json north_star): eviction sequences, eviction counts and
+cache-hit decisions bit-exact; TTFT/E2E within 1e-9 relative in fp64 — we
+assert the stronger bit-exact equality (tolerance 0) on every per-request
+field.  Sizes are chosen so the oracle finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import (assert_report_equal, assert_summaries_equal, ref_catalog, ref_scenario, ref_trace)
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2506_18796_b200")
+from paper_2506_18796_b200 import api, synth  # noqa: E402
+from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig, Variant  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if P.device_count() < 1:
+        pytest.fail("no CUDA device visible: the GPU tests must run on a B200 (no CPU fallback)")
+
+
+def _replay_and_compare(ref, catalog, traces, sc, ctx=""):
+    rcat = ref_catalog(ref, catalog)
+    summ, reps = P.run_batch(traces, catalog, sc, dump_scenarios=list(range(len(sc))), raise_on_error=False)
+    for k in range(len(sc)):
+        want = ref.run(rcat, ref_trace(traces[int(sc[k]["trace"])]), ref_scenario(ref, sc[k]))
+        assert_report_equal(reps[k], want, f"{ctx} scenario {k} {sc[k]}")
+    return summ
+
+
+def test_device_log_bit_exact_vs_libm(ref):
+    rng = np.random.default_rng(7)
+    x = np.concatenate([
+        np.exp(rng.uniform(0.0, 25.0, 4_000_000)),          # t = clock - last_used >= 1, wide
+        1.0 + rng.uniform(0.0, 0.0647, 1_000_000),          # the near-1 polynomial path
+        np.array([1.0, 1.0 + 2**-52, 1.0647, 1.06469, 2.0, 1e300, 1e-300, 5e-324]),
+        np.arange(1, 200_001, dtype=np.float64),             # integer-second idle times
+    ])
+    got = api.device_log(x)
+    want = ref.libm_log(x)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
+    assert len(bad) == 0, f"{len(bad)} mismatches, e.g. x={x[bad[:4]]}"
+
+
+def test_config2_cace_vs_lru_bit_exact(ref):
+    """BASELINE config 2: same 10k trace, CACE vs LRU, 8 CodeLLMs, budget fits 3."""
+    catalog, traces, sc = synth.config2(n_requests=10_000, seed=1)
+    summ = _replay_and_compare(ref, catalog, traces, sc, "cfg2")
+    assert summ["evictions"][0] < summ["evictions"][1]  # CACE evicts less than LRU here
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_scenarios_bit_exact(ref, seed):
+    """Random traces x every variant / P1 mode / window / capacity / w1 / unload."""
+    rng = np.random.default_rng(100 + seed)
+    catalog = synth.eight_model_catalog() if seed % 2 == 0 else api.ModelCatalog.build_default()
+    traces = [synth.mixed_trace(catalog, int(rng.integers(50, 3000)), seed=1000 * seed + k,
+                                rate=float(rng.choice([0.2, 1.0, 3.0, 10.0, 40.0])), bursty=bool(k % 2))
+              for k in range(3)]
+    rows = []
+    for _ in range(40):
+        pol = PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.choice([0.0, 0.25, 0.5, 1.0, 1.7])),
+                           window_length=int(rng.choice([1, 2, 3, 5, 10, 16, 50, 200])),
+                           output_token_normalizer=int(rng.choice([600, 300, 50])),
+                           p1_mode=int(rng.integers(0, 2)))
+        cl = ClusterConfig(num_accelerators=int(rng.integers(1, 9)), models_per_accelerator=1,
+                           unload_time_s=float(rng.choice([0.0, 0.0, 0.5, 2.0])))
+        rows.append((int(rng.integers(0, 3)), pol, cl))
+    sc = api.make_scenarios(rows)
+    _replay_and_compare(ref, catalog, traces, sc, f"seed{seed}")
+
+
+def test_reference_build_trace_grid_bit_exact(ref):
+    """Traces from the reference's own generator (build_trace, all 3 patterns)."""
+    rcat = ref.Catalog.default()
+    catalog = api.ModelCatalog.build_default()
+    traces = []
+    for pat, rate, seed in ((0, 15.0, 1), (1, 15.0, 2), (2, 4.0, 3), (1, 10.0, 7)):
+        t = ref.build_trace(rcat, pat, rate, 30.0, seed)
+        traces.append(api.Trace(t["arrival"], t["model"], t["prompt"], t["output"]))
+    rows = []
+    for ti in range(len(traces)):
+        for v in range(6):
+            rows.append((ti, PolicyConfig(variant=v, w1=0.5, window_length=10), ClusterConfig()))
+            rows.append((ti, PolicyConfig(variant=v, w1=1.0, window_length=2), ClusterConfig(num_accelerators=3)))
+    _replay_and_compare(ref, catalog, traces, api.make_scenarios(rows), "build_trace")
+
+
+def test_batch_summaries_match_reference_fanout(ref):
+    """Summary mode (hashes of every outcome and of the eviction sequence) vs
+    the reference run() fanned out over threads, 256 scenarios x 20k requests."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 20_000, seed=s) for s in (3, 4)]
+    pols = synth.weight_vectors_cfg3()[::32]  # 128 vectors over all variants / modes / windows
+    sc = synth.scenario_grid(pols, [2, 3], 1, catalog.max_expected_output_tokens())
+    sc = np.concatenate([sc, sc.copy()])
+    sc["trace"][len(sc) // 2:] = 1
+    got = P.run_batch(traces, catalog, sc)
+    rcat = ref_catalog(ref, catalog)
+    want, _ = ref.run_batch(rcat, [ref_trace(t) for t in traces], [ref_scenario(ref, s) for s in sc])
+    assert_summaries_equal(got, want, "batch")
+
+
+def test_unsorted_trace_and_equal_arrivals(ref):
+    """run() pops arrivals by (time, index); the engine stable-sorts and maps back."""
+    catalog = synth.eight_model_catalog()
+    rng = np.random.default_rng(5)
+    n = 800
+    arr = np.round(rng.uniform(0, 60, n), 1)  # many exact ties, unsorted
+    t = api.Trace(arr, rng.integers(0, 8, n), np.full(n, 256), np.full(n, 50))
+    rows = [(0, PolicyConfig(variant=v, window_length=w), ClusterConfig(num_accelerators=c))
+            for v in range(6) for w in (1, 4) for c in (1, 3)]
+    _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "unsorted")
+
+
+def test_simultaneous_completions_push_order(ref):
+    """Same-time ServiceCompletes must pop in push (seq) order (engine.cpp:49-55)."""
+    catalog = synth.eight_model_catalog()
+    # integer-ish arrivals and identical service times produce exact time ties
+    n = 600
+    arr = np.repeat(np.arange(n // 3, dtype=np.float64) * 0.5, 3)
+    model = np.tile(np.array([0, 2, 4, 6, 1, 3], np.int32), n // 6)
+    t = api.Trace(arr, model, np.full(n, 256), np.full(n, 64))
+    rows = [(0, PolicyConfig(variant=v, window_length=3), ClusterConfig(num_accelerators=c))
+            for v in range(6) for c in (2, 3, 4, 6)]
+    _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "ties")
+
+
+def test_error_paths_match_reference_messages(ref):
+    catalog = synth.eight_model_catalog()
+    t = synth.mixed_trace(catalog, 100, seed=1)
+    rcat = ref_catalog(ref, catalog)
+    cases = [
+        (PolicyConfig(window_length=0), ClusterConfig(), api.SimError),
+        (PolicyConfig(), ClusterConfig(num_accelerators=0), api.SimError),
+        (PolicyConfig(), ClusterConfig(models_per_accelerator=0), api.SimError),
+    ]
+    for pol, cl, exc in cases:
+        sc = api.make_scenarios([(0, pol, cl)])
+        with pytest.raises(exc) as ei:
+            P.run(t, catalog, cl, pol)
+        with pytest.raises(ref.RefError) as er:
+            ref.run(rcat, ref_trace(t), ref_scenario(ref, sc[0]))
+        assert str(ei.value) == str(er.value)
+
+
+def test_empty_trace(ref):
+    catalog = synth.eight_model_catalog()
+    t = api.Trace(np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32))
+    rep = P.run(t, catalog)
+    assert rep.counters.hits == 0 and rep.counters.misses == 0 and rep.max_resident == 0
+
+
+# ---- reference unit tests, restated against the GPU engine (test_engine.cpp) ----
+
+def _req(at, lang, tc, prompt=256, output=50):
+    return (at, lang, tc, prompt, output)
+
+
+def test_cold_start_closed_form():  # test_engine.cpp:70-86
+    cat = api.ModelCatalog.build_default()
+    t = api.Trace.from_requests(cat, [_req(1.0, 0, 0)])
+    rep = P.run(t, cat, ClusterConfig(), PolicyConfig(variant=Variant.LRU))
+    m = cat.models[cat.lookup(0, 0)]
+    assert rep.cold_start[0] and rep.counters.misses == 1 and rep.loads == 1
+    assert rep.counters.load_overhead_s == m.load_time_s
+    assert rep.ttft_s[0] == m.load_time_s + rep.prefill_s[0]
+    assert rep.e2e_s[0] == rep.ttft_s[0] + rep.decode_s[0]
+
+
+def test_warm_hit():  # test_engine.cpp:88-100
+    cat = api.ModelCatalog.build_default()
+    t = api.Trace.from_requests(cat, [_req(0.0, 0, 0), _req(20.0, 0, 0)])
+    rep = P.run(t, cat, ClusterConfig(), PolicyConfig(variant=Variant.LRU))
+    assert rep.counters.hits == 1 and rep.counters.misses == 1 and not rep.cold_start[1]
+    assert rep.ttft_s[1] == rep.prefill_s[1]
+
+
+def test_capacity_sufficient_never_evicts():  # test_engine.cpp:102-121
+    cat = api.ModelCatalog.build_default()
+    langs = [0, 1, 4, 5]
+    t = api.Trace.from_requests(cat, [_req(i * 3.0, langs[i % 4], 0) for i in range(40)])
+    for v in range(6):
+        rep = P.run(t, cat, ClusterConfig(), PolicyConfig(variant=v, output_token_normalizer=600))
+        assert rep.counters.evictions == 0 and rep.counters.misses == 4 and rep.counters.hits == 36
+        assert rep.max_resident <= 4
+
+
+def test_lru_thrash_vs_cace_window():  # test_engine.cpp:123-152
+    cat = api.ModelCatalog.build_default()
+    langs = [0, 1, 4, 5]
+    t = api.Trace.from_requests(cat, [_req(i * 0.01, langs[i % 4], 0) for i in range(40)])
+    cl = ClusterConfig(num_accelerators=3)
+    lru = P.run(t, cat, cl, PolicyConfig(variant=Variant.LRU))
+    cace = P.run(t, cat, cl, PolicyConfig(variant=Variant.CACE_FULL, window_length=2))
+    hr = lambda r: r.counters.hits / (r.counters.hits + r.counters.misses)
+    assert hr(cace) > hr(lru) and hr(cace) > 0
+
+
+def test_unload_delay():  # test_engine.cpp:185-200
+    cat = api.ModelCatalog.build_default()
+    t = api.Trace.from_requests(cat, [_req(0.0, 0, 0), _req(0.1, 1, 0)])
+    a = P.run(t, cat, ClusterConfig(num_accelerators=1), PolicyConfig(variant=Variant.LRU))
+    b = P.run(t, cat, ClusterConfig(num_accelerators=1, unload_time_s=2.0), PolicyConfig(variant=Variant.LRU))
+    assert a.counters.evictions == 1 and b.counters.evictions == 1
+    assert abs(b.ttft_s[1] - (a.ttft_s[1] + 2.0)) < 1e-12
+
+
+def test_conservation_invariants():  # test_engine.cpp:154-183 / acceptance criterion 6
+    cat = synth.eight_model_catalog()
+    rng = np.random.default_rng(777)
+    for i in range(30):
+        t = synth.mixed_trace(cat, int(rng.integers(10, 400)), seed=50000 + i, rate=float(1 + 19 * rng.random()))
+        pol = PolicyConfig(variant=i % 6, w1=float(rng.random()), window_length=1 + int(rng.integers(0, 15)))
+        rep = P.run(t, cat, ClusterConfig(), pol)
+        assert rep.counters.hits + rep.counters.misses == len(t)
+        assert rep.loads == rep.counters.misses and rep.max_resident <= 4
+        assert np.all(np.abs(rep.e2e_s - (rep.ttft_s + rep.decode_s)) <= 1e-9)
+        lt = np.array([m.load_time_s for m in cat.models])
+        assert abs(rep.counters.load_overhead_s - lt[t.model[rep.cold_start]].sum()) <= 1e-6
+
+
+# ---- policy-level entry points vs the reference (test_policy.cpp) ----
+
+def test_select_victim_bruteforce_vs_reference(ref):
+    """2,000 randomized ResidencySets per test_policy.cpp:160-258 / acceptance criterion 4."""
+    cat = api.ModelCatalog.build_default()
+    rcat = ref.Catalog.default()
+    rng = np.random.default_rng(2024)
+    inst, want = [], []
+    for it in range(2000):
+        k = 2 + int(rng.integers(0, 3))
+        picks = rng.choice(len(cat), k, replace=False)
+        clock = 10.0 + 90.0 * rng.random()
+        ents = []
+        for idx in picks:
+            busy = rng.integers(0, 4) == 0
+            lu = 5.0 if rng.integers(0, 3) == 0 else clock * rng.random()
+            ents.append((int(idx), float(lu), bool(busy)))
+        wl = 1 + int(rng.integers(0, 12))
+        pending = rng.integers(0, len(cat), int(rng.integers(0, 12)))
+        win = ref.dedup_window(rcat, pending, wl)
+        pol = PolicyConfig(variant=it % 6, w1=(it % 5) * 0.5, window_length=wl, p1_mode=it % 2)
+        inst.append((ents, list(win), clock, pol))
+        rs = ref.scenario(variant=pol.variant, p1_mode=pol.p1_mode, window_length=wl, w1=pol.w1)
+        want.append(ref.select_victim(rcat, [e[0] for e in ents], [e[1] for e in ents], [e[2] for e in ents],
+                                      win, wl, clock, rs))
+    got = api.select_victim(cat, inst)
+    assert np.array_equal(got, np.array(want)), np.nonzero(got != np.array(want))[0][:10]
+
+
+def test_eviction_score_bits_vs_reference(ref):
+    cat = api.ModelCatalog.build_default()
+    rcat = ref.Catalog.default()
+    rng = np.random.default_rng(9)
+    inst, want = [], []
+    for it in range(3000):
+        m = int(rng.integers(0, 16))
+        clock = float(rng.uniform(0, 500))
+        lu = float(clock - rng.choice([0.0, 0.5, 1.0, rng.uniform(0, 400)]))
+        wl = 1 + int(rng.integers(0, 12))
+        win = ref.dedup_window(rcat, rng.integers(0, 16, int(rng.integers(0, 12))), wl)
+        pol = PolicyConfig(variant=int(rng.integers(1, 6)), w1=float(rng.uniform(0, 2)), window_length=wl,
+                           p1_mode=int(rng.integers(0, 2)), output_token_normalizer=int(rng.choice([600, 50, 7])))
+        inst.append((m, lu, list(win), clock, pol))
+        want.append(ref.eviction_score(rcat, m, lu, win, wl, clock,
+                                       ref.scenario(variant=pol.variant, p1_mode=pol.p1_mode, window_length=wl,
+                                                    w1=pol.w1, output_token_normalizer=pol.output_token_normalizer)))
+    got = api.eviction_score(cat, inst)
+    assert np.array_equal(got.view(np.uint64), np.array(want).view(np.uint64))
+
+
+def test_eviction_score_spot_values():  # test_policy.cpp:37-96, acceptance criterion 5
+    cat = api.ModelCatalog.build_default()
+    jc = cat.index_of("java-completion")
+    base = PolicyConfig(variant=Variant.CACE_FULL, w1=1.0, window_length=10, output_token_normalizer=600)
+    out = api.eviction_score(cat, [
+        (jc, 0.0, [], 10.0, base),
+        (jc, 0.0, [cat.index_of("go-reasoning")], 10.0, base),
+        (jc, 0.0, [jc, cat.index_of("go-reasoning")], 10.0, base),
+        (jc, 0.0, [cat.index_of("go-reasoning"), jc], 10.0, base),
+        (jc, 10.0, [], 10.0, PolicyConfig(p1_mode=1)),
+        (jc, 9.5, [], 10.0, PolicyConfig(p1_mode=1)),
+        (jc, 0.0, [], 50.0, PolicyConfig(p1_mode=0)),
+        (jc, 0.0, [], 50.0, PolicyConfig(p1_mode=1)),
+        (jc, 0.0, [], 10.0, PolicyConfig(w1=0.5)),
+    ])
+    assert out[1, 2] == 1.0 and out[2, 2] == 0.0 and abs(out[3, 2] - 0.1) < 1e-12
+    assert out[4, 0] == 1.0 and out[5, 0] == 1.0
+    assert abs(out[6, 0] + out[7, 0] - 1.0) < 1e-12
+    assert abs(out[7, 0] - 1.0 / (1.0 + np.log(50.0))) < 1e-15
+    assert abs(out[8, 3] - 0.5 * 50.0 / 600.0) < 1e-15
+    with pytest.raises(api.SimError, match="clock precedes last_used_s for java-completion"):
+        api.eviction_score(cat, [(jc, 20.0, [], 10.0, base)])
+
+
+def test_select_victim_busy_and_lru_tie():  # test_policy.cpp:129-158
+    cat = api.ModelCatalog.build_default()
+    i = cat.index_of
+    lru = PolicyConfig(variant=Variant.LRU)
+    got = api.select_victim(cat, [
+        ([(i("java-completion"), 1.0, True), (i("python-completion"), 2.0, False)], [], 10.0, lru),
+        ([(i("java-completion"), 1.0, True), (i("python-completion"), 2.0, True)], [], 10.0, lru),
+        ([(i("python-completion"), 3.0, False), (i("go-reasoning"), 3.0, False), (i("java-reasoning"), 5.0, False)],
+         [], 10.0, lru),
+    ])
+    assert list(got) == [i("python-completion"), -1, i("go-reasoning")]
+
+
+def test_dedup_window_and_service_times():  # test_policy.cpp:22-35, test_engine.cpp:43-68
+    w = api.dedup_window([[0, 1, 0, 2, 1, 3, 4], [0, 1, 0, 2, 1, 3, 4], []], [5, 2, 10])
+    assert [list(x) for x in w] == [[0, 1, 2], [0, 1], []]
+    with pytest.raises(api.SimError, match="dedup_window: length must be >= 1"):
+        api.dedup_window([[0]], [0])
+    cat = api.ModelCatalog([api.ModelDescriptor("x", 0, 0, 1, 1, 1.0, 1024.0, 100.0, 1)])
+    pf, dc = api.service_times(cat, [0, 0], [256, 256], [50, 0])
+    assert pf[0] == 0.25 and dc[0] == 0.5 and dc[1] == 1.0 / 100.0
