@@ -61,18 +61,6 @@ def workload(args):
     return catalog, traces, sc
 
 
-def shard_bounds(sc, world):
-    """Cost-balanced contiguous shards: cost ~ n * (1 + c*w) per scenario
-    (SURVEY §8e), approximated by 1 + log2(w)/8 + C/8."""
-    cost = 1.0 + np.log2(np.maximum(sc["window_length"], 1)) / 8.0 + sc["num_accelerators"] / 8.0
-    cum = np.concatenate([[0.0], np.cumsum(cost)])
-    bounds = [0]
-    for r in range(1, world):
-        bounds.append(int(np.searchsorted(cum, cum[-1] * r / world)))
-    bounds.append(len(sc))
-    return bounds
-
-
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -198,11 +186,16 @@ def main():
     from paper_2506_18796_b200 import SUMMARY_DTYPE
 
     catalog, traces, sc_all = workload(args)
+    from paper_2506_18796_b200.shard import shard_bounds
+
     bounds = shard_bounds(sc_all, world)
     sc = sc_all[bounds[rank]:bounds[rank + 1]]
     S_total = len(sc_all)
     n_req = args.requests
-    stream = torch.cuda.current_stream()
+    # A dedicated (non-default) stream: the engine, the events and the L2
+    # flush all run on it, so the CUDA events bracket exactly the replay.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng = P.Engine(catalog, traces, device=local, stream=stream.cuda_stream)
     eng.plan(sc)
     d_sc = torch.from_numpy(sc.view(np.uint8).copy()).cuda()

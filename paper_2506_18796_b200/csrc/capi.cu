@@ -142,7 +142,7 @@ struct Catalog {
   DBuf<int32_t> d_lex;
 
   void load(const cace_catalog_t* c) {
-    if (!c || c->n_models < 1 || c->n_models > 65535 || !c->load_time_s || !c->prefill_rate_tps ||
+    if (!c || c->n_models < 1 || c->n_models > 65534 || !c->load_time_s || !c->prefill_rate_tps ||
         !c->decode_rate_tps || !c->expected_output_tokens || !c->lex_rank || !c->task_class)
       throw Invalid{CACE_E_INVALID, "cace: malformed catalog"};
     M = c->n_models;
@@ -201,11 +201,15 @@ struct cace_engine {
   DBuf<int64_t> d_bad_idx;
   DBuf<int32_t> d_bad_code;
   int last_launches = 0;
+  std::vector<cudaStream_t> workers;  // fork/join streams for capacity segments
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork = nullptr;
 };
 
 namespace {
 
 constexpr int kMaxLaneC = 16;
+constexpr int kWorkers = 8;
 
 void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trace_t* traces,
                   int32_t n_traces, const cace_opts_t* opts) {
@@ -218,6 +222,15 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
     e->own_stream = true;
   }
   e->log_variant = resolve_log_variant(opts);
+  for (int k = 0; k < kWorkers; ++k) {
+    cudaStream_t ws;
+    cudaEvent_t ev;
+    CK(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    e->workers.push_back(ws);
+    e->joins.push_back(ev);
+  }
+  CK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   e->cat.load(catalog);
   const int M = e->cat.M;
   if (n_traces < 0 || (n_traces > 0 && !traces)) throw Invalid{CACE_E_INVALID, "cace: bad traces"};
@@ -346,23 +359,21 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C>
+template <int C, bool DUMP>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
-  static bool attr_set = false;  // per-process; smem need is bounded by M
-  if (smem > 48 * 1024 && !attr_set) {
-    CK(cudaFuncSetAttribute(replay_lane_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            227 * 1024));
-    attr_set = true;
-  }
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(replay_lane_kernel<C, DUMP>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
-  replay_lane_kernel<C><<<grid, LANE_BLOCK, smem, s>>>(P);
+  replay_lane_kernel<C, DUMP><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 
+template <bool DUMP>
 void dispatch_lane(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   switch (C) {
 #define CASE(k) \
-  case k: launch_lane<k>(P, count, smem, s); break;
+  case k: launch_lane<k, DUMP>(P, count, smem, s); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
@@ -389,11 +400,30 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   P.dump = dump;
   const size_t smem = lane_smem_bytes(e->cat.M);
   e->last_launches = 0;
-  for (const auto& g : e->segs) {
-    P.seg_begin = g.b;
-    P.seg_end = g.e;
-    dispatch_lane(g.C, P, g.e - g.b, smem, s);
-    ++e->last_launches;
+  // Capacity segments are independent kernels: fork them over the engine's
+  // worker streams so they share the SMs (one segment alone is often less
+  // than a wave), then join back onto s.
+  const bool dump_on = dump.slot != nullptr;
+  const size_t nseg = e->segs.size();
+  if (nseg > 0) {
+    CK(cudaEventRecord(e->fork, s));
+    for (size_t k = 0; k < nseg; ++k) {
+      cudaStream_t ws = nseg == 1 ? s : e->workers[k % e->workers.size()];
+      if (ws != s) CK(cudaStreamWaitEvent(ws, e->fork, 0));
+      const auto& g = e->segs[k];
+      P.seg_begin = g.b;
+      P.seg_end = g.e;
+      if (dump_on)
+        dispatch_lane<true>(g.C, P, g.e - g.b, smem, ws);
+      else
+        dispatch_lane<false>(g.C, P, g.e - g.b, smem, ws);
+      ++e->last_launches;
+    }
+    if (nseg > 1)
+      for (size_t k = 0; k < std::min(nseg, e->workers.size()); ++k) {
+        CK(cudaEventRecord(e->joins[k], e->workers[k]));
+        CK(cudaStreamWaitEvent(s, e->joins[k], 0));
+      }
   }
   if (!e->bad_idx.empty()) {
     fill_status_kernel<<<(unsigned)((e->bad_idx.size() + 255) / 256), 256, 0, s>>>(
@@ -468,6 +498,12 @@ void cace_engine_destroy(cace_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
+  for (auto ws : e->workers) {
+    cudaStreamSynchronize(ws);
+    cudaStreamDestroy(ws);
+  }
+  for (auto ev : e->joins) cudaEventDestroy(ev);
+  if (e->fork) cudaEventDestroy(e->fork);
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }

@@ -98,10 +98,62 @@ __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf,
   mc = q1.w;
 }
 
-// Replays one scenario.  first/p4 are this lane's shared-memory columns
-// (element m at [m * stride]).  Template C = capacity (slots), so the slot
-// arrays live in registers with fully unrolled scans.
+// Per-lane replay state for one scenario.  Template C = capacity (slots):
+// the slot arrays live in registers with fully unrolled scans.
 template <int C>
+struct Lane {
+  // slots: model | state << 16, last_used, ServiceComplete time + push seq
+  int sms[C];
+  double slu[C], sdone[C];
+  uint32_t sseq[C];
+  int occ;
+  int ls;          // slot with the in-flight load (-1 none)
+  double lready;   // its LoadComplete time
+  uint32_t seqc;   // ServiceComplete push order
+  // queue head (first unserved request, replay order)
+  uint32_t head;
+  double ha, hpf, hdc, hlw;
+  uint32_t hnxt, hmc;
+  bool hc, hcold, harr;
+  double now;
+  // results
+  uint32_t hits, misses, evictions, loads, nc, nr;
+  double lo_sum, sttft, se2e, mttft, me2e;
+  uint64_t ho, he;
+  int status;
+};
+
+__device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
+__device__ __forceinline__ int slot_state(int v) { return v >> 16; }
+
+// start_load (engine.cpp:123-132): the head's model into `target`.
+template <int C>
+__device__ __forceinline__ void start_load(Lane<C>& L, int target, double udelay, const double* s_lt) {
+  const int hm = (int)(L.hmc & 0xffffu);
+  const double lt = s_lt[hm];
+  const double ready = (L.now + udelay) + lt;
+  L.hlw = ready - L.now;
+  L.lo_sum += lt;
+  ++L.loads;
+#pragma unroll
+  for (int s = 0; s < C; ++s)
+    if (s == target) {
+      L.sms[s] = hm | (ST_LOADING << 16);
+      L.slu[s] = L.now;
+    }
+  L.ls = target;
+  L.lready = ready;
+}
+
+// Replays one scenario.  Two phases per iteration so the expensive part runs
+// converged across the warp:
+//   A (divergent, cheap): events + head-of-line dispatch (hits, service
+//     starts, free-slot loads) until the lane reaches an eviction decision
+//     or finishes;
+//   B (converged): the eviction decision — victim selection over the idle
+//     residents (policy.cpp:80-115) and the load that follows.
+// first/p4 are this lane's shared-memory columns (element m at [m*stride]).
+template <int C, bool DUMP>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* first,
                                 double* p4tab, int stride, const double* s_lt,
                                 const double* s_p2, const int* s_lex) {
@@ -116,13 +168,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
   const bool verbatim = sc.p1_mode == CACE_P1_VERBATIM;
   const uint32_t w = (uint32_t)sc.window_length;
   const double wd = (double)sc.window_length;
-  const double unload = sc.unload_time_s;
 
-  // Dump slot (rare; only for full-report scenarios).
   int dslot = -1;
-  if (P.dump.slot) dslot = P.dump.slot[sidx];
-  const int64_t doff = dslot >= 0 ? P.dump.dump_off[dslot] : 0;
-  int64_t dn_ev = 0;
+  int64_t doff = 0, dn_ev = 0;
+  if (DUMP) {
+    dslot = P.dump.slot[sidx];
+    if (dslot >= 0) doff = P.dump.dump_off[dslot];
+  }
 
   if (need_win) {
     const uint32_t* f0 = P.first0 + (int64_t)sc.trace * M;
@@ -134,303 +186,291 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
     for (int m = 0; m < M; ++m) p4tab[m * stride] = sc.w1 * (__ldg(P.cat.tokens + m) / norm);
   }
 
-  // Slot state (registers).
-  int sm[C];
-  int sst[C];
-  double slu[C], sdone[C];
-  uint32_t sseq[C];
+  Lane<C> L;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
-    sm[s] = -1;
-    sst[s] = ST_IDLE;
-    slu[s] = 0.0;
-    sdone[s] = 0.0;
-    sseq[s] = 0;
+    L.sms[s] = 0xffff;  // empty
+    L.slu[s] = 0.0;
+    L.sdone[s] = 0.0;
+    L.sseq[s] = 0;
   }
-  int occ = 0;
-  int ls = -1;          // slot with the in-flight load
-  double lready = 0.0;  // its LoadComplete time
-  uint32_t seqc = 0;    // ServiceComplete push order
+  L.occ = 0;
+  L.ls = -1;
+  L.lready = 0.0;
+  L.seqc = 0;
+  L.head = 0;
+  L.ha = L.hpf = L.hdc = L.hlw = 0.0;
+  L.hnxt = L.hmc = 0;
+  L.hc = L.hcold = L.harr = false;
+  L.now = 0.0;
+  L.hits = L.misses = L.evictions = L.loads = L.nc = L.nr = 0;
+  L.lo_sum = L.sttft = L.se2e = L.mttft = L.me2e = 0.0;
+  L.ho = L.he = CACE_HASH_SEED;
+  L.status = CACE_OK;
+  if (n > 0) load_rec(tr, L.ha, L.hpf, L.hdc, L.hnxt, L.hmc);
 
-  uint64_t hits = 0, misses = 0, evictions = 0, loads = 0;
-  double lo_sum = 0.0;
-  uint64_t nc = 0, nr = 0;
-  double sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
-  uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
-  int status = CACE_OK;
-
-  // Queue head.
-  uint32_t head = 0;
-  double ha = 0.0, hpf = 0.0, hdc = 0.0, hlw = 0.0;
-  uint32_t hnxt = 0, hmc = 0;
-  bool hc = false, hcold = false, harr = false;
-  if (n > 0) load_rec(tr, ha, hpf, hdc, hnxt, hmc);
-
-  while (head < n) {
-    // ---- next completion event: min (time, kind, seq) over the load and
-    // the busy slots (engine.cpp:49-55).
-    double tc = 0.0;
-    int sc_slot = -1;
-    bool cload = false;
-    uint32_t qc = 0;
-    if (ls >= 0) {
-      tc = lready;
-      sc_slot = ls;
-      cload = true;
-    }
+  bool active = n > 0;
+  bool need_dec = false;
+  for (;;) {
+    // ================= phase A: cheap, divergent =================
+    while (active && !need_dec) {
+      // next completion: min (time, kind, seq) over the load and the busy
+      // slots (engine.cpp:49-55)
+      double tc = L.lready;
+      int sc_slot = L.ls;
+      bool cload = L.ls >= 0;
+      uint32_t qc = 0;
 #pragma unroll
-    for (int s = 0; s < C; ++s) {
-      const bool busy = sst[s] == ST_BUSY;
-      const bool better =
-          busy && (sc_slot < 0 || sdone[s] < tc || (sdone[s] == tc && !cload && sseq[s] < qc));
-      if (better) {
-        tc = sdone[s];
-        sc_slot = s;
-        cload = false;
-        qc = sseq[s];
-      }
-    }
-    double now;
-    if (!harr && (sc_slot < 0 || ha < tc)) {
-      // Arrival of the head into an empty queue.
-      now = ha;
-      harr = true;
-    } else if (sc_slot < 0) {
-      status = CACE_E_DEADLOCK;  // pending requests, nothing schedulable
-      break;
-    } else {
-      // LoadComplete / ServiceComplete: slot -> Idle, last_used = event time
-      // (engine.cpp:219-230).
-      now = tc;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (s == sc_slot) {
-          sst[s] = ST_IDLE;
-          slu[s] = now;
+      for (int s = 0; s < C; ++s) {
+        const bool better = slot_state(L.sms[s]) == ST_BUSY &&
+                            (sc_slot < 0 || L.sdone[s] < tc ||
+                             (L.sdone[s] == tc && !cload && L.sseq[s] < qc));
+        if (better) {
+          tc = L.sdone[s];
+          sc_slot = s;
+          cload = false;
+          qc = L.sseq[s];
         }
-      if (cload) ls = -1;
-      if (!harr) continue;  // queue empty: dispatch has nothing to do
-    }
-
-    // ---- dispatch(now): head-of-line FIFO (engine.cpp:157-210).
-    for (;;) {
-      const int hm = (int)(hmc & 0xffffu);
-      int hs = -1;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (sm[s] == hm) hs = s;
-      int hst = ST_IDLE;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (s == hs) hst = sst[s];
-      if (!hc) {  // classify once (engine.cpp:163-173)
-        hc = true;
-        const bool hit = hs >= 0 && hst != ST_LOADING;
-        hits += hit ? 1 : 0;
-        misses += hit ? 0 : 1;
-        hcold = !hit;
       }
-      if (hs >= 0) {
-        if (hst != ST_IDLE) break;  // busy or still loading
-        // start_service (engine.cpp:134-153)
-        const double qd = now - ha;
-        const double ttft = qd + hpf;
-        const double e2e = ttft + hdc;
-        const double done = (now + hpf) + hdc;
+      if (!L.harr && (sc_slot < 0 || L.ha < tc)) {
+        L.now = L.ha;  // arrival of the head into an empty queue
+        L.harr = true;
+      } else if (sc_slot < 0) {
+        L.status = CACE_E_DEADLOCK;  // pending requests, nothing schedulable
+        active = false;
+        break;
+      } else {
+        // Load/ServiceComplete: slot -> Idle, last_used = event time
+        // (engine.cpp:219-230)
+        L.now = tc;
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if (s == hs) {
-            sst[s] = ST_BUSY;
-            sdone[s] = done;
-            sseq[s] = seqc;
+          if (s == sc_slot) {
+            L.sms[s] = slot_model(L.sms[s]);  // state ST_IDLE == 0
+            L.slu[s] = tc;
           }
-        ++seqc;
-        if ((hmc >> 16) == CACE_COMPLETION) {
-          ++nc;
-          sttft += ttft;
-          mttft = ttft > mttft ? ttft : mttft;
-        } else {
-          ++nr;
-          se2e += e2e;
-          me2e = e2e > me2e ? e2e : me2e;
-        }
-        ho = hmix(hmix(ho, dbits(ttft)), dbits(e2e) ^ (hcold ? 1ull : 0ull));
-        if (dslot >= 0) {
-          const int64_t o = doff + P.perm[base + head];
-          if (P.dump.cold) P.dump.cold[o] = hcold ? 1 : 0;
-          if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - hlw;
-          if (P.dump.load_wait) P.dump.load_wait[o] = hlw;
-          if (P.dump.prefill) P.dump.prefill[o] = hpf;
-          if (P.dump.decode) P.dump.decode[o] = hdc;
-          if (P.dump.ttft) P.dump.ttft[o] = ttft;
-          if (P.dump.e2e) P.dump.e2e[o] = e2e;
-        }
-        // pop the head; the next one is pending iff it arrived before now.
-        if (need_win) first[hm * stride] = hnxt;
-        ++head;
-        if (head == n) break;
-        load_rec(tr + head, ha, hpf, hdc, hnxt, hmc);
-        hc = false;
-        hcold = false;
-        hlw = 0.0;
-        harr = ha < now;
-        if (!harr) break;
-        continue;
+        if (cload) L.ls = -1;
+        if (!L.harr) continue;  // queue empty: dispatch has nothing to do
       }
 
-      int target;
-      double udelay;
-      if (occ < C) {  // free slot: load without unload delay (engine.cpp:184-187)
-        target = occ;
-        ++occ;
-        udelay = 0.0;
-      } else {
-        // ---- victim selection among idle residents (policy.cpp:80-115).
-        // Sorted-first = min (last_used, lex) over idle = the LRU victim.
-        int f = -1;
-        double flu = 0.0;
-        int flex = 0;
+      // dispatch(now): head-of-line FIFO (engine.cpp:157-210)
+      for (;;) {
+        const int hm = (int)(L.hmc & 0xffffu);
+        int hs = -1, hst = ST_IDLE;
 #pragma unroll
-        for (int s = 0; s < C; ++s) {
-          if (sst[s] != ST_IDLE) continue;
-          const int lx = s_lex[sm[s]];
-          if (f < 0 || slu[s] < flu || (slu[s] == flu && lx < flex)) {
-            f = s;
-            flu = slu[s];
-            flex = lx;
+        for (int s = 0; s < C; ++s)
+          if (slot_model(L.sms[s]) == hm) {
+            hs = s;
+            hst = slot_state(L.sms[s]);
           }
+        if (!L.hc) {  // classify once (engine.cpp:163-173)
+          L.hc = true;
+          const bool hit = hs >= 0 && hst != ST_LOADING;
+          L.hits += hit ? 1u : 0u;
+          L.misses += hit ? 0u : 1u;
+          L.hcold = !hit;
         }
-        if (f < 0) break;  // every resident busy: wait (engine.cpp:203)
-        int victim = f;
-        if (!is_lru) {
-          // Score every idle entry; "first strict max in sorted order".
-          double tot[C];
-          int bad_lex = 1 << 30, bad_model = -1;
+        if (hs >= 0) {
+          if (hst != ST_IDLE) break;  // busy or still loading
+          // start_service (engine.cpp:134-153)
+          const double qd = L.now - L.ha;
+          const double ttft = qd + L.hpf;
+          const double e2e = ttft + L.hdc;
+          const double done = (L.now + L.hpf) + L.hdc;
 #pragma unroll
-          for (int s = 0; s < C; ++s) {
-            tot[s] = 0.0;
-            if (sst[s] != ST_IDLE) continue;
-            const int m = sm[s];
-            if (now < slu[s]) {  // eviction_score throws (policy.cpp:43-46)
-              const int lx = s_lex[m];
-              if (lx < bad_lex) {
-                bad_lex = lx;
-                bad_model = m;
-              }
+          for (int s = 0; s < C; ++s)
+            if (s == hs) {
+              L.sms[s] = hm | (ST_BUSY << 16);
+              L.sdone[s] = done;
+              L.sseq[s] = L.seqc;
             }
-            double p1 = 0.0;
-            if (variant != CACE_MINUS_P1) {
-              const double d = now - slu[s];
-              const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
-              const double L = cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
-              const double p1v = 1.0 / (1.0 + L);
-              p1 = verbatim ? p1v : 1.0 - p1v;
-            }
-            const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[m];
-            double p3 = 0.0;
-            if (variant != CACE_MINUS_P3) {
-              const uint32_t fm = first[m * stride];
-              // in window [head, min(head + w, arrived)): fm >= head always
-              bool inwin = fm < n && fm - head < w;
-              if (inwin) inwin = __ldg(&tr[fm].arrival) < now;
-              if (inwin) {
-                int rank = 0;
-                for (int mm = 0; mm < M; ++mm) rank += first[mm * stride] < fm ? 1 : 0;
-                p3 = (double)rank / wd;
-              } else {
-                p3 = 1.0;
-              }
-            }
-            const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[m * stride];
-            tot[s] = ((p1 + p2) + p3) + p4;
+          ++L.seqc;
+          if ((L.hmc >> 16) == CACE_COMPLETION) {
+            ++L.nc;
+            L.sttft += ttft;
+            L.mttft = ttft > L.mttft ? ttft : L.mttft;
+          } else {
+            ++L.nr;
+            L.se2e += e2e;
+            L.me2e = e2e > L.me2e ? e2e : L.me2e;
           }
-          if (bad_model >= 0) {
-            status = CACE_E_CLOCK | (bad_model << 8);
+          L.ho = hmix(hmix(L.ho, dbits(ttft)), dbits(e2e) ^ (L.hcold ? 1ull : 0ull));
+          if (DUMP && dslot >= 0) {
+            const int64_t o = doff + P.perm[base + L.head];
+            if (P.dump.cold) P.dump.cold[o] = L.hcold ? 1 : 0;
+            if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - L.hlw;
+            if (P.dump.load_wait) P.dump.load_wait[o] = L.hlw;
+            if (P.dump.prefill) P.dump.prefill[o] = L.hpf;
+            if (P.dump.decode) P.dump.decode[o] = L.hdc;
+            if (P.dump.ttft) P.dump.ttft[o] = ttft;
+            if (P.dump.e2e) P.dump.e2e[o] = e2e;
+          }
+          // pop the head; the next is pending iff it arrived before now
+          if (need_win) first[hm * stride] = L.hnxt;
+          ++L.head;
+          if (L.head == n) {
+            active = false;
             break;
           }
+          load_rec(tr + L.head, L.ha, L.hpf, L.hdc, L.hnxt, L.hmc);
+          L.hc = false;
+          L.hcold = false;
+          L.hlw = 0.0;
+          L.harr = L.ha < L.now;
+          if (!L.harr) break;
+          continue;
+        }
+        if (L.occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
+          start_load(L, L.occ, 0.0, s_lt);
+          ++L.occ;
+          break;
+        }
+        bool any_idle = false;
+#pragma unroll
+        for (int s = 0; s < C; ++s) any_idle |= slot_state(L.sms[s]) == ST_IDLE;
+        need_dec = any_idle;  // else every resident busy: wait (engine.cpp:203)
+        break;
+      }
+    }
+
+    // ================= phase B: eviction decision, converged =================
+    if (need_dec) {
+      need_dec = false;
+      const double now = L.now;
+      // Sorted-first = min (last_used, lex) over idle residents = LRU victim.
+      int f = -1;
+      double flu = 0.0;
+      int flex = 0;
+#pragma unroll
+      for (int s = 0; s < C; ++s) {
+        const int lx = s_lex[slot_model(L.sms[s])];
+        if (slot_state(L.sms[s]) == ST_IDLE &&
+            (f < 0 || L.slu[s] < flu || (L.slu[s] == flu && lx < flex))) {
+          f = s;
+          flu = L.slu[s];
+          flex = lx;
+        }
+      }
+      int victim = f;
+      if (!is_lru) {
+        // eviction_score for every idle entry (policy.cpp:39-78); the
+        // victim is the first strict max in sorted order.
+        uint32_t fm[C];
+#pragma unroll
+        for (int s = 0; s < C; ++s) fm[s] = need_win ? first[slot_model(L.sms[s]) * stride] : 0u;
+        int rank[C];
+#pragma unroll
+        for (int s = 0; s < C; ++s) rank[s] = 0;
+        if (need_win) {
+          for (int mm = 0; mm < M; ++mm) {
+            const uint32_t x = first[mm * stride];
+#pragma unroll
+            for (int s = 0; s < C; ++s) rank[s] += x < fm[s] ? 1 : 0;
+          }
+        }
+        double tot[C];
+        int bad_lex = 1 << 30, bad_model = -1;
+#pragma unroll
+        for (int s = 0; s < C; ++s) {
+          const int m = slot_model(L.sms[s]);
+          const bool idle = slot_state(L.sms[s]) == ST_IDLE;
+          if (idle && now < L.slu[s]) {  // eviction_score throws (policy.cpp:43-46)
+            const int lx = s_lex[m];
+            if (lx < bad_lex) {
+              bad_lex = lx;
+              bad_model = m;
+            }
+          }
+          double p1 = 0.0;
+          if (variant != CACE_MINUS_P1) {
+            const double d = now - L.slu[s];
+            const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
+            const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
+            const double p1v = 1.0 / (1.0 + lg);
+            p1 = verbatim ? p1v : 1.0 - p1v;
+          }
+          const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[m];
+          double p3 = 0.0;
+          if (variant != CACE_MINUS_P3) {
+            // in window [head, min(head + w, arrived)); fm >= head always
+            bool inwin = fm[s] < n && fm[s] - L.head < w;
+            if (inwin) inwin = __ldg(&tr[fm[s]].arrival) < now;
+            p3 = inwin ? (double)rank[s] / wd : 1.0;
+          }
+          const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[m * stride];
+          tot[s] = ((p1 + p2) + p3) + p4;
+        }
+        if (bad_model >= 0) {
+          L.status = CACE_E_CLOCK | (bad_model << 8);
+          active = false;
+        } else {
           double bt = 0.0;
 #pragma unroll
           for (int s = 0; s < C; ++s)
             if (s == f) bt = tot[s];
-          if (bt == bt) {  // sorted-first NaN keeps it; NaN never wins later
+          if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
             int blex = flex;
             double blu = flu;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              if (sst[s] != ST_IDLE || s == f) continue;
-              const double ts = tot[s];
-              const int lx = s_lex[sm[s]];
-              const bool earlier = slu[s] < blu || (slu[s] == blu && lx < blex);
-              if (ts > bt || (ts == bt && earlier)) {
+              const int lx = s_lex[slot_model(L.sms[s])];
+              const bool earlier = L.slu[s] < blu || (L.slu[s] == blu && lx < blex);
+              if (slot_state(L.sms[s]) == ST_IDLE && s != f &&
+                  (tot[s] > bt || (tot[s] == bt && earlier))) {
                 victim = s;
-                bt = ts;
-                blu = slu[s];
+                bt = tot[s];
+                blu = L.slu[s];
                 blex = lx;
               }
             }
           }
         }
+      }
+      if (active) {
         int vm = -1;
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if (s == victim) vm = sm[s];
-        ++evictions;  // residents.erase(victim) (engine.cpp:205-206)
-        he = hmix(hmix(he, (uint64_t)vm), dbits(now));
-        if (dslot >= 0) {
+          if (s == victim) vm = slot_model(L.sms[s]);
+        ++L.evictions;  // residents.erase(victim) (engine.cpp:205-206)
+        L.he = hmix(hmix(L.he, (uint64_t)vm), dbits(now));
+        if (DUMP && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
             if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = now;
           }
           ++dn_ev;
         }
-        target = victim;
-        udelay = unload;
+        start_load(L, victim, sc.unload_time_s, s_lt);
       }
-      // start_load (engine.cpp:123-132)
-      const double lt = s_lt[hm];
-      const double ready = (now + udelay) + lt;
-      hlw = ready - now;
-      lo_sum += lt;
-      ++loads;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (s == target) {
-          sm[s] = hm;
-          sst[s] = ST_LOADING;
-          slu[s] = now;
-        }
-      ls = target;
-      lready = ready;
-      break;
     }
-    if (status != CACE_OK) break;
+    if (!active) break;
   }
 
   cace_summary_t o;
-  o.hits = hits;
-  o.misses = misses;
-  o.evictions = evictions;
-  o.loads = loads;
-  o.load_overhead_s = lo_sum;
-  o.max_resident = occ;
-  o.status = status;
-  o.n_completion = nc;
-  o.n_reasoning = nr;
-  o.sum_ttft_completion = sttft;
-  o.sum_e2e_reasoning = se2e;
-  o.max_ttft_completion = mttft;
-  o.max_e2e_reasoning = me2e;
-  o.eviction_hash = he;
-  o.outcome_hash = ho;
+  o.hits = L.hits;
+  o.misses = L.misses;
+  o.evictions = L.evictions;
+  o.loads = L.loads;
+  o.load_overhead_s = L.lo_sum;
+  o.max_resident = L.occ;
+  o.status = L.status;
+  o.n_completion = L.nc;
+  o.n_reasoning = L.nr;
+  o.sum_ttft_completion = L.sttft;
+  o.sum_e2e_reasoning = L.se2e;
+  o.max_ttft_completion = L.mttft;
+  o.max_e2e_reasoning = L.me2e;
+  o.eviction_hash = L.he;
+  o.outcome_hash = L.ho;
   P.out[sidx] = o;
-  if (dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
+  if (DUMP && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
 }
 
 // Block of LANE_BLOCK lanes; per-lane shared columns for first[] and p4[],
 // block-shared copy of the hot catalog columns.
 constexpr int LANE_BLOCK = 128;
 
-template <int C>
+template <int C, bool DUMP>
 __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = P.cat.M;
@@ -447,8 +487,8 @@ __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P)
   __syncthreads();
   const int64_t gi = P.seg_begin + (int64_t)blockIdx.x * LANE_BLOCK + threadIdx.x;
   if (gi >= P.seg_end) return;
-  replay_scenario<C>(P, P.order[gi], first + threadIdx.x, p4tab + threadIdx.x, LANE_BLOCK, s_lt,
-                     s_p2, s_lex);
+  replay_scenario<C, DUMP>(P, P.order[gi], first + threadIdx.x, p4tab + threadIdx.x, LANE_BLOCK,
+                           s_lt, s_p2, s_lex);
 }
 
 inline size_t lane_smem_bytes(int M) {
