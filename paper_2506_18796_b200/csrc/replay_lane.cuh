@@ -123,12 +123,16 @@ struct Lane {
   int status;
 };
 
+// Slot word: model (bits 0-15) | state (16-17) | lex rank of model_id (18-31).
 __device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
-__device__ __forceinline__ int slot_state(int v) { return v >> 16; }
+__device__ __forceinline__ int slot_state(int v) { return (v >> 16) & 3; }
+__device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
+__device__ __forceinline__ int with_state(int v, int st) { return (v & ~(3 << 16)) | (st << 16); }
 
 // start_load (engine.cpp:123-132): the head's model into `target`.
 template <int C>
-__device__ __forceinline__ void start_load(Lane<C>& L, int target, double udelay, const double* s_lt) {
+__device__ __forceinline__ void start_load(Lane<C>& L, int target, double udelay, const double* s_lt,
+                                           const int* s_lex) {
   const int hm = (int)(L.hmc & 0xffffu);
   const double lt = s_lt[hm];
   const double ready = (L.now + udelay) + lt;
@@ -138,7 +142,7 @@ __device__ __forceinline__ void start_load(Lane<C>& L, int target, double udelay
 #pragma unroll
   for (int s = 0; s < C; ++s)
     if (s == target) {
-      L.sms[s] = hm | (ST_LOADING << 16);
+      L.sms[s] = hm | (ST_LOADING << 16) | (s_lex[hm] << 18);
       L.slu[s] = L.now;
     }
   L.ls = target;
@@ -246,7 +250,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
 #pragma unroll
         for (int s = 0; s < C; ++s)
           if (s == sc_slot) {
-            L.sms[s] = slot_model(L.sms[s]);  // state ST_IDLE == 0
+            L.sms[s] = with_state(L.sms[s], ST_IDLE);
             L.slu[s] = tc;
           }
         if (cload) L.ls = -1;
@@ -280,7 +284,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
 #pragma unroll
           for (int s = 0; s < C; ++s)
             if (s == hs) {
-              L.sms[s] = hm | (ST_BUSY << 16);
+              L.sms[s] = with_state(L.sms[s], ST_BUSY);
               L.sdone[s] = done;
               L.sseq[s] = L.seqc;
             }
@@ -321,7 +325,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
           continue;
         }
         if (L.occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
-          start_load(L, L.occ, 0.0, s_lt);
+          start_load(L, L.occ, 0.0, s_lt, s_lex);
           ++L.occ;
           break;
         }
@@ -343,7 +347,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
       int flex = 0;
 #pragma unroll
       for (int s = 0; s < C; ++s) {
-        const int lx = s_lex[slot_model(L.sms[s])];
+        const int lx = slot_lex(L.sms[s]);
         if (slot_state(L.sms[s]) == ST_IDLE &&
             (f < 0 || L.slu[s] < flu || (L.slu[s] == flu && lx < flex))) {
           f = s;
@@ -353,14 +357,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
       }
       int victim = f;
       if (!is_lru) {
-        // eviction_score for every idle entry (policy.cpp:39-78); the
-        // victim is the first strict max in sorted order.
+        // eviction_score for every idle entry (policy.cpp:39-78); the victim
+        // is the first strict max in sorted order.
         uint32_t fm[C];
-#pragma unroll
-        for (int s = 0; s < C; ++s) fm[s] = need_win ? first[slot_model(L.sms[s]) * stride] : 0u;
         int rank[C];
 #pragma unroll
-        for (int s = 0; s < C; ++s) rank[s] = 0;
+        for (int s = 0; s < C; ++s) {
+          fm[s] = need_win ? first[slot_model(L.sms[s]) * stride] : 0u;
+          rank[s] = 0;
+        }
         if (need_win) {
           for (int mm = 0; mm < M; ++mm) {
             const uint32_t x = first[mm * stride];
@@ -368,59 +373,114 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
             for (int s = 0; s < C; ++s) rank[s] += x < fm[s] ? 1 : 0;
           }
         }
-        double tot[C];
-        int bad_lex = 1 << 30, bad_model = -1;
+        bool inwin[C];
+        bool bad_clock = false;
+#pragma unroll
+        for (int s = 0; s < C; ++s) {
+          bool iw = false;
+          if (variant != CACE_MINUS_P3) {
+            // in window [head, min(head + w, arrived)); fm >= head always
+            iw = fm[s] < n && fm[s] - L.head < w;
+            if (iw) iw = __ldg(&tr[fm[s]].arrival) < now;
+          }
+          inwin[s] = iw;
+          bad_clock |= slot_state(L.sms[s]) == ST_IDLE && now < L.slu[s];
+        }
+        // ---- screening pass in fp32 with a rigorous error bound: if one
+        // candidate's approximate total beats every other by more than the
+        // bound, it is the exact arg-max and the fp64 totals are not needed.
+        // |T~ - T| <= 2.6e-5 (3-ulp __logf on ln t < 70, Lipschitz-1 P1) plus
+        // fp32 rounding of the terms and sums (<= 2^-22 |T|); margin 2x that.
+        float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
+        int bs = -1;
+        bool exact = bad_clock;
+        const float wf = (float)sc.window_length;
 #pragma unroll
         for (int s = 0; s < C; ++s) {
           const int m = slot_model(L.sms[s]);
-          const bool idle = slot_state(L.sms[s]) == ST_IDLE;
-          if (idle && now < L.slu[s]) {  // eviction_score throws (policy.cpp:43-46)
-            const int lx = s_lex[m];
-            if (lx < bad_lex) {
-              bad_lex = lx;
-              bad_model = m;
-            }
-          }
-          double p1 = 0.0;
+          float p1 = 0.0f;
           if (variant != CACE_MINUS_P1) {
             const double d = now - L.slu[s];
-            const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
-            const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
-            const double p1v = 1.0 / (1.0 + lg);
-            p1 = verbatim ? p1v : 1.0 - p1v;
+            const double t = d < 1.0 ? 1.0 : d;
+            exact |= !(t < 1e30);
+            const float p1v = __frcp_rn(1.0f + __logf((float)t));
+            p1 = verbatim ? p1v : 1.0f - p1v;
           }
-          const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[m];
-          double p3 = 0.0;
-          if (variant != CACE_MINUS_P3) {
-            // in window [head, min(head + w, arrived)); fm >= head always
-            bool inwin = fm[s] < n && fm[s] - L.head < w;
-            if (inwin) inwin = __ldg(&tr[fm[s]].arrival) < now;
-            p3 = inwin ? (double)rank[s] / wd : 1.0;
+          const float p2 = variant == CACE_MINUS_P2 ? 0.0f : (float)s_p2[m];
+          const float p3 =
+              variant == CACE_MINUS_P3 ? 0.0f : (inwin[s] ? __fdiv_rn((float)rank[s], wf) : 1.0f);
+          const float p4 = variant == CACE_MINUS_P4 ? 0.0f : (float)p4tab[m * stride];
+          const float T = ((p1 + p2) + p3) + p4;
+          if (slot_state(L.sms[s]) == ST_IDLE) {
+            tmax = fmaxf(tmax, fabsf(T));
+            exact |= !(fabsf(T) <= 1e6f);  // NaN / inf / huge: decide exactly
+            if (T > best) {
+              second = best;
+              best = T;
+              bs = s;
+            } else if (T > second) {
+              second = T;
+            }
           }
-          const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[m * stride];
-          tot[s] = ((p1 + p2) + p3) + p4;
         }
-        if (bad_model >= 0) {
-          L.status = CACE_E_CLOCK | (bad_model << 8);
-          active = false;
-        } else {
-          double bt = 0.0;
+        const float margin = 6e-5f + 4.8e-7f * tmax;
+        exact |= !(best - second > margin);
+        victim = bs;
+        if (exact) {
+          // ---- exact fp64 path (policy.cpp:39-115), bit-identical to the
+          // reference: needed for near-ties (3-11% of CACE decisions are
+          // exact ties broken by last_used, then model_id).
+          double tot[C];
+          int bad_lex = 1 << 30, bad_model = -1;
 #pragma unroll
-          for (int s = 0; s < C; ++s)
-            if (s == f) bt = tot[s];
-          if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
-            int blex = flex;
-            double blu = flu;
+          for (int s = 0; s < C; ++s) {
+            tot[s] = 0.0;
+            if (slot_state(L.sms[s]) != ST_IDLE) continue;
+            const int m = slot_model(L.sms[s]);
+            if (now < L.slu[s]) {  // eviction_score throws (policy.cpp:43-46)
+              const int lx = slot_lex(L.sms[s]);
+              if (lx < bad_lex) {
+                bad_lex = lx;
+                bad_model = m;
+              }
+            }
+            double p1 = 0.0;
+            if (variant != CACE_MINUS_P1) {
+              const double d = now - L.slu[s];
+              const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
+              const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
+              const double p1v = 1.0 / (1.0 + lg);
+              p1 = verbatim ? p1v : 1.0 - p1v;
+            }
+            const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[m];
+            const double p3 =
+                variant == CACE_MINUS_P3 ? 0.0 : (inwin[s] ? (double)rank[s] / wd : 1.0);
+            const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[m * stride];
+            tot[s] = ((p1 + p2) + p3) + p4;
+          }
+          if (bad_model >= 0) {
+            L.status = CACE_E_CLOCK | (bad_model << 8);
+            active = false;
+          } else {
+            victim = f;
+            double bt = 0.0;
 #pragma unroll
-            for (int s = 0; s < C; ++s) {
-              const int lx = s_lex[slot_model(L.sms[s])];
-              const bool earlier = L.slu[s] < blu || (L.slu[s] == blu && lx < blex);
-              if (slot_state(L.sms[s]) == ST_IDLE && s != f &&
-                  (tot[s] > bt || (tot[s] == bt && earlier))) {
-                victim = s;
-                bt = tot[s];
-                blu = L.slu[s];
-                blex = lx;
+            for (int s = 0; s < C; ++s)
+              if (s == f) bt = tot[s];
+            if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
+              int blex = flex;
+              double blu = flu;
+#pragma unroll
+              for (int s = 0; s < C; ++s) {
+                const int lx = slot_lex(L.sms[s]);
+                const bool earlier = L.slu[s] < blu || (L.slu[s] == blu && lx < blex);
+                if (slot_state(L.sms[s]) == ST_IDLE && s != f &&
+                    (tot[s] > bt || (tot[s] == bt && earlier))) {
+                  victim = s;
+                  bt = tot[s];
+                  blu = L.slu[s];
+                  blex = lx;
+                }
               }
             }
           }
@@ -440,7 +500,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
           }
           ++dn_ev;
         }
-        start_load(L, victim, sc.unload_time_s, s_lt);
+        start_load(L, victim, sc.unload_time_s, s_lt, s_lex);
       }
     }
     if (!active) break;
