@@ -16,6 +16,7 @@
 #include "glibc_log.cuh"
 #include "policy_kernels.cuh"
 #include "replay_lane.cuh"
+#include "layout.hpp"
 
 using namespace cace;
 
@@ -42,11 +43,6 @@ struct CudaFail {
     if (e_ != cudaSuccess)                                                        \
       throw CudaFail{CACE_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
-
-struct Invalid {
-  int32_t code;
-  std::string what;
-};
 
 // Device buffer owned by RAII.
 template <typename T>
@@ -127,41 +123,10 @@ void require_device(const cace_opts_t* o) {
   CK(cudaSetDevice(dev));
 }
 
-std::string model_name(const std::vector<std::string>& ids, int m) {
-  if (m >= 0 && m < (int)ids.size() && !ids[m].empty()) return ids[m];
-  return "model#" + std::to_string(m);
-}
-
-// Host copy of the catalog + device columns.
-struct Catalog {
-  int M = 0;
-  std::vector<double> lt, pr, dr, tok, p2;
-  std::vector<int32_t> lex, cls;
-  std::vector<std::string> ids;
+// Host catalog + its device columns.
+struct Catalog : HostCatalog {
   DBuf<double> d_lt, d_p2, d_tok;
   DBuf<int32_t> d_lex;
-
-  void load(const cace_catalog_t* c) {
-    if (!c || c->n_models < 1 || c->n_models > 65534 || !c->load_time_s || !c->prefill_rate_tps ||
-        !c->decode_rate_tps || !c->expected_output_tokens || !c->lex_rank || !c->task_class)
-      throw Invalid{CACE_E_INVALID, "cace: malformed catalog"};
-    M = c->n_models;
-    lt.assign(c->load_time_s, c->load_time_s + M);
-    pr.assign(c->prefill_rate_tps, c->prefill_rate_tps + M);
-    dr.assign(c->decode_rate_tps, c->decode_rate_tps + M);
-    tok.resize(M);
-    p2.resize(M);
-    for (int m = 0; m < M; ++m) {
-      tok[m] = (double)c->expected_output_tokens[m];
-      p2[m] = 1.0 / (1.0 + lt[m] / 100.0);  // policy.cpp:55
-    }
-    lex.assign(c->lex_rank, c->lex_rank + M);
-    cls.assign(c->task_class, c->task_class + M);
-    ids.assign(M, std::string());
-    if (c->model_id)
-      for (int m = 0; m < M; ++m)
-        if (c->model_id[m]) ids[m] = c->model_id[m];
-  }
   void upload(cudaStream_t s) {
     d_lt.upload(lt.data(), M, s);
     d_p2.upload(p2.data(), M, s);
@@ -169,7 +134,6 @@ struct Catalog {
     d_lex.upload(lex.data(), M, s);
   }
   DevCatalog dev() const { return DevCatalog{M, d_lt.p, d_p2.p, d_tok.p, d_lex.p}; }
-  bool bad_rates(int m) const { return pr[m] <= 0 || dr[m] <= 0; }  // engine.cpp:17
 };
 
 }  // namespace
@@ -181,9 +145,7 @@ struct cace_engine {
   bool own_stream = false;
   int log_variant = CACE_LOG_FMA;
   Catalog cat;
-  int T = 0;
-  std::vector<int64_t> off;        // [T+1]
-  std::vector<int32_t> bad_model;  // [T] first (sorted) request model with bad rates, or -1
+  HostLayout lay;  // host replay-order layout (rec/perm/first0 freed after upload)
   DBuf<ReqRec> d_rec;
   DBuf<int64_t> d_off;
   DBuf<uint32_t> d_first0, d_perm;
@@ -208,7 +170,6 @@ struct cace_engine {
 
 namespace {
 
-constexpr int kMaxLaneC = 16;
 constexpr int kWorkers = 8;
 
 void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -232,85 +193,18 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
   }
   CK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   e->cat.load(catalog);
-  const int M = e->cat.M;
-  if (n_traces < 0 || (n_traces > 0 && !traces)) throw Invalid{CACE_E_INVALID, "cace: bad traces"};
-  e->T = n_traces;
-  e->off.assign(n_traces + 1, 0);
-  for (int t = 0; t < n_traces; ++t) {
-    if (traces[t].n_requests < 0 || traces[t].n_requests > 0xfffffff0LL)
-      throw Invalid{CACE_E_INVALID, "cace: trace too long"};
-    e->off[t + 1] = e->off[t] + traces[t].n_requests;
-  }
-  const int64_t N = e->off[n_traces];
-  std::vector<ReqRec> rec(N);
-  std::vector<uint32_t> perm(N), first0((size_t)n_traces * M);
-  e->bad_model.assign(n_traces, -1);
-  std::vector<uint32_t> last(M);
-  for (int t = 0; t < n_traces; ++t) {
-    const cace_trace_t& tr = traces[t];
-    const int64_t n = tr.n_requests, b = e->off[t];
-    if (n > 0 && (!tr.arrival_time_s || !tr.model || !tr.prompt_tokens || !tr.output_tokens))
-      throw Invalid{CACE_E_INVALID, "cace: trace arrays missing"};
-    // run() resolves every request's model first (engine.cpp:87-92).
-    for (int64_t i = 0; i < n; ++i) {
-      const int m = tr.model[i];
-      if (m < 0 || m >= M)
-        throw Invalid{CACE_E_LOOKUP, "catalog: no model registered for model index " +
-                                         std::to_string(m)};
-      if (!std::isfinite(tr.arrival_time_s[i]))
-        throw Invalid{CACE_E_INVALID, "cace: non-finite arrival_time_s"};
-    }
-    // Replay order = Arrival pop order (time, seq=index) (engine.cpp:49-55).
-    std::vector<uint32_t> ord(n);
-    std::iota(ord.begin(), ord.end(), 0u);
-    bool sorted = true;
-    for (int64_t i = 1; i < n && sorted; ++i)
-      sorted = !(tr.arrival_time_s[i] < tr.arrival_time_s[i - 1]);
-    if (!sorted)
-      std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
-        return tr.arrival_time_s[x] < tr.arrival_time_s[y];
-      });
-    for (int m = 0; m < M; ++m) last[m] = (uint32_t)n;
-    for (int64_t k = n - 1; k >= 0; --k) {
-      const uint32_t i = ord[k];
-      const int m = tr.model[i];
-      ReqRec& r = rec[b + k];
-      r.arrival = tr.arrival_time_s[i];
-      // service_times (engine.cpp:15-26)
-      r.prefill = (double)tr.prompt_tokens[i] / e->cat.pr[m];
-      r.decode = (double)std::max(tr.output_tokens[i], 1) / e->cat.dr[m];
-      r.nxt = last[m];
-      r.mc = (uint32_t)m | ((uint32_t)(e->cat.cls[m] == CACE_REASONING) << 16);
-      last[m] = (uint32_t)k;
-      perm[b + k] = i;
-      if (e->cat.bad_rates(m)) e->bad_model[t] = m;  // ends as the first in replay order
-    }
-    for (int m = 0; m < M; ++m) first0[(size_t)t * M + m] = last[m];
-  }
+  build_layout(e->cat, traces, n_traces, e->lay);
   cudaStream_t s = e->stream;
   e->cat.upload(s);
-  e->d_rec.upload(rec.data(), N, s);
-  e->d_off.upload(e->off.data(), e->off.size(), s);
-  e->d_first0.upload(first0.data(), first0.size(), s);
-  e->d_perm.upload(perm.data(), perm.size(), s);
+  e->d_rec.upload(e->lay.rec.data(), e->lay.rec.size(), s);
+  e->d_off.upload(e->lay.off.data(), e->lay.off.size(), s);
+  e->d_first0.upload(e->lay.first0.data(), e->lay.first0.size(), s);
+  e->d_perm.upload(e->lay.perm.data(), e->lay.perm.size(), s);
   e->d_tab.upload(kLogTab, 256, s);
   e->d_tab2.upload(kLogTab2, 256, s);
   CK(cudaStreamSynchronize(s));
-}
-
-// Reference run() preconditions (engine.cpp:79-92, 17-20) per scenario.
-int32_t precheck(const cace_engine* e, const cace_scenario_t& sc) {
-  if (sc.trace < 0 || sc.trace >= e->T) return CACE_E_INVALID;
-  if (sc.variant < CACE_LRU || sc.variant > CACE_MINUS_P4) return CACE_E_INVALID;
-  if (sc.window_length < 1) return CACE_E_WINDOW;
-  if (sc.num_accelerators < 1) return CACE_E_ACCELERATORS;
-  const int64_t n = e->off[sc.trace + 1] - e->off[sc.trace];
-  if (n == 0) return CACE_OK;
-  if (e->bad_model[sc.trace] >= 0) return CACE_E_RATES | (e->bad_model[sc.trace] << 8);
-  const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
-  if (cap < 1) return CACE_E_DEADLOCK;  // nothing can ever load (engine.cpp:235-237)
-  if (cap > kMaxLaneC) return CACE_E_INVALID;
-  return CACE_OK;
+  std::vector<ReqRec>().swap(e->lay.rec);  // device copy is authoritative
+  std::vector<uint32_t>().swap(e->lay.perm);
 }
 
 void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
@@ -321,9 +215,9 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   std::vector<int64_t> ok;
   ok.reserve(n);
   for (int64_t i = 0; i < n; ++i) {
-    const int32_t st = precheck(e, sc[i]);
-    const int64_t len = e->off[sc[i].trace >= 0 && sc[i].trace < e->T ? sc[i].trace + 1 : 0] -
-                        e->off[sc[i].trace >= 0 && sc[i].trace < e->T ? sc[i].trace : 0];
+    const int32_t st = precheck(e->lay, sc[i]);
+    const bool tv = sc[i].trace >= 0 && sc[i].trace < e->lay.T;
+    const int64_t len = tv ? e->lay.off[sc[i].trace + 1] - e->lay.off[sc[i].trace] : 0;
     if (st != CACE_OK || len == 0) {
       e->bad_idx.push_back(i);
       e->bad_code.push_back(st);
@@ -433,22 +327,6 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   }
 }
 
-std::string status_text(const cace_engine* e, int32_t status) {
-  const int code = status & 0xff;
-  const int m = status >> 8;
-  switch (code) {
-    case CACE_OK: return "";
-    case CACE_E_WINDOW: return "run: window_length must be >= 1";
-    case CACE_E_ACCELERATORS: return "run: need at least one accelerator";
-    case CACE_E_RATES: return "service_times: rates must be positive for " + model_name(e->cat.ids, m);
-    case CACE_E_CLOCK:
-      return "eviction_score: clock precedes last_used_s for " + model_name(e->cat.ids, m);
-    case CACE_E_DEADLOCK: return "run: deadlock \xe2\x80\x94 pending requests with no schedulable event";
-    case CACE_E_RESIDENCY: return "run: residency bound violated";
-    default: return "cace: invalid scenario (bad trace index, variant, or capacity > 16)";
-  }
-}
-
 template <typename F>
 int32_t guarded(char* msg, size_t cap, F&& f) {
   try {
@@ -532,7 +410,7 @@ int32_t cace_engine_replay_device(cace_engine* e, const cace_scenario_t* d_scena
 int32_t cace_engine_status_message(const cace_engine* e, int32_t status, char* msg,
                                    size_t msg_cap) {
   if (!e) return CACE_E_INVALID;
-  put_msg(msg, msg_cap, status_text(e, status));
+  put_msg(msg, msg_cap, status_text(e->cat, status));
   return status & 0xff;
 }
 
@@ -571,7 +449,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
         slot[si] = k;
         doff.push_back(total);
         const int t = scenarios[si].trace;
-        total += (t >= 0 && t < e->T) ? e->off[t + 1] - e->off[t] : 0;
+        total += (t >= 0 && t < e->lay.T) ? e->lay.off[t + 1] - e->lay.off[t] : 0;
       }
       d_slot.upload(slot.data(), slot.size(), s);
       d_doff.upload(doff.data(), doff.size(), s);
@@ -627,7 +505,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
     CK(cudaStreamSynchronize(s));
     for (int64_t i = 0; i < n_scenarios; ++i) {
       if (summaries[i].status != CACE_OK) {
-        put_msg(msg, msg_cap, status_text(e, summaries[i].status));
+        put_msg(msg, msg_cap, status_text(e->cat, summaries[i].status));
         return summaries[i].status & 0xff;
       }
     }

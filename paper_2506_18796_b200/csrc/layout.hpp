@@ -1,0 +1,184 @@
+// Host-side preparation shared by the C ABI (capi.cu) and the test-only host
+// emulation build: catalog validation, the replay-order trace layout
+// (ReqRec records, next-same-model links, per-model first occurrences) and the
+// reference run() preconditions per scenario.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cace_gpu.h"
+#include "replay_types.h"
+
+namespace cace {
+
+struct Invalid {
+  int32_t code;
+  std::string what;
+};
+
+inline std::string model_name(const std::vector<std::string>& ids, int m) {
+  if (m >= 0 && m < (int)ids.size() && !ids[m].empty()) return ids[m];
+  return "model#" + std::to_string(m);
+}
+
+constexpr int kMaxLaneC = 16;  // capacities the lane kernel is instantiated for
+
+// Host copy of the catalog columns the replay reads (catalog.hpp:13-25).
+struct HostCatalog {
+  int M = 0;
+  std::vector<double> lt, pr, dr, tok, p2;
+  std::vector<int32_t> lex, cls;
+  std::vector<std::string> ids;
+
+  void load(const cace_catalog_t* c) {
+    if (!c || c->n_models < 1 || c->n_models > 16383 || !c->load_time_s || !c->prefill_rate_tps ||
+        !c->decode_rate_tps || !c->expected_output_tokens || !c->lex_rank || !c->task_class)
+      throw Invalid{CACE_E_INVALID, "cace: malformed catalog"};
+    M = c->n_models;
+    for (int m = 0; m < M; ++m) {
+      // catalog.cpp:49 rejects load_time_s <= 0; infinite times/rates would
+      // make the event clock non-monotone, which the engine does not model.
+      if (!(c->load_time_s[m] > 0) || !std::isfinite(c->load_time_s[m]))
+        throw Invalid{CACE_E_INVALID, "catalog: load_time_s must be positive and finite"};
+      if (std::isinf(c->prefill_rate_tps[m]) || std::isinf(c->decode_rate_tps[m]) ||
+          std::isnan(c->prefill_rate_tps[m]) || std::isnan(c->decode_rate_tps[m]))
+        throw Invalid{CACE_E_INVALID, "catalog: prefill/decode rates must be finite"};
+      if (c->lex_rank[m] < 0 || c->lex_rank[m] >= M)
+        throw Invalid{CACE_E_INVALID, "cace: lex_rank out of range"};
+    }
+    lt.assign(c->load_time_s, c->load_time_s + M);
+    pr.assign(c->prefill_rate_tps, c->prefill_rate_tps + M);
+    dr.assign(c->decode_rate_tps, c->decode_rate_tps + M);
+    tok.resize(M);
+    p2.resize(M);
+    for (int m = 0; m < M; ++m) {
+      tok[m] = (double)c->expected_output_tokens[m];
+      p2[m] = 1.0 / (1.0 + lt[m] / 100.0);  // policy.cpp:55
+    }
+    lex.assign(c->lex_rank, c->lex_rank + M);
+    cls.assign(c->task_class, c->task_class + M);
+    ids.assign(M, std::string());
+    if (c->model_id)
+      for (int m = 0; m < M; ++m)
+        if (c->model_id[m]) ids[m] = c->model_id[m];
+  }
+  bool bad_rates(int m) const { return pr[m] <= 0 || dr[m] <= 0; }  // engine.cpp:17
+};
+
+// Replay-order layout of all traces, concatenated.
+struct HostLayout {
+  int T = 0;
+  std::vector<int64_t> off;        // [T+1]
+  std::vector<ReqRec> rec;         // [N] sorted by (arrival, index)
+  std::vector<uint32_t> perm;      // [N] sorted position -> caller's request index
+  std::vector<uint32_t> first0;    // [T][M] first sorted index of each model (n if absent)
+  std::vector<int32_t> bad_model;  // [T] model of the first request with bad rates, or -1
+};
+
+inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int32_t n_traces,
+                         HostLayout& L) {
+  const int M = cat.M;
+  if (n_traces < 0 || (n_traces > 0 && !traces)) throw Invalid{CACE_E_INVALID, "cace: bad traces"};
+  L.T = n_traces;
+  L.off.assign(n_traces + 1, 0);
+  for (int t = 0; t < n_traces; ++t) {
+    if (traces[t].n_requests < 0 || traces[t].n_requests > 0xfffffff0LL)
+      throw Invalid{CACE_E_INVALID, "cace: trace too long"};
+    L.off[t + 1] = L.off[t] + traces[t].n_requests;
+  }
+  const int64_t N = L.off[n_traces];
+  L.rec.assign(N, ReqRec{});
+  L.perm.assign(N, 0);
+  L.first0.assign((size_t)n_traces * M, 0);
+  L.bad_model.assign(n_traces, -1);
+  std::vector<uint32_t> last(M);
+  for (int t = 0; t < n_traces; ++t) {
+    const cace_trace_t& tr = traces[t];
+    const int64_t n = tr.n_requests, b = L.off[t];
+    if (n > 0 && (!tr.arrival_time_s || !tr.model || !tr.prompt_tokens || !tr.output_tokens))
+      throw Invalid{CACE_E_INVALID, "cace: trace arrays missing"};
+    // run() resolves every request's model first (engine.cpp:87-92).
+    for (int64_t i = 0; i < n; ++i) {
+      const int m = tr.model[i];
+      if (m < 0 || m >= M)
+        throw Invalid{CACE_E_LOOKUP,
+                      "catalog: no model registered for model index " + std::to_string(m)};
+      if (!std::isfinite(tr.arrival_time_s[i]))
+        throw Invalid{CACE_E_INVALID, "cace: non-finite arrival_time_s"};
+      if (tr.prompt_tokens[i] < 0)  // a negative prefill would run the event clock backwards
+        throw Invalid{CACE_E_INVALID, "cace: negative prompt_tokens"};
+    }
+    // Replay order = Arrival pop order (time, seq = index) (engine.cpp:49-55).
+    std::vector<uint32_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0u);
+    bool sorted = true;
+    for (int64_t i = 1; i < n && sorted; ++i)
+      sorted = !(tr.arrival_time_s[i] < tr.arrival_time_s[i - 1]);
+    if (!sorted)
+      std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
+        return tr.arrival_time_s[x] < tr.arrival_time_s[y];
+      });
+    for (int m = 0; m < M; ++m) last[m] = (uint32_t)n;
+    for (int64_t k = n - 1; k >= 0; --k) {
+      const uint32_t i = ord[k];
+      const int m = tr.model[i];
+      ReqRec& r = L.rec[b + k];
+      r.arrival = tr.arrival_time_s[i];
+      // service_times (engine.cpp:15-26)
+      r.prefill = (double)tr.prompt_tokens[i] / cat.pr[m];
+      r.decode = (double)std::max(tr.output_tokens[i], 1) / cat.dr[m];
+      r.nxt = last[m];
+      r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
+      last[m] = (uint32_t)k;
+      L.perm[b + k] = i;
+      if (cat.bad_rates(m)) L.bad_model[t] = m;  // ends as the first in replay order
+    }
+    for (int m = 0; m < M; ++m) L.first0[(size_t)t * M + m] = last[m];
+  }
+}
+
+// Reference run() preconditions (engine.cpp:79-92, 17-20) for one scenario:
+// the SimError it would raise (code | model << 8), CACE_OK, or CACE_E_INVALID
+// for inputs outside the engine's domain.
+inline int32_t precheck(const HostLayout& L, const cace_scenario_t& sc) {
+  if (sc.trace < 0 || sc.trace >= L.T) return CACE_E_INVALID;
+  if (sc.variant < CACE_LRU || sc.variant > CACE_MINUS_P4) return CACE_E_INVALID;
+  if (sc.window_length < 1) return CACE_E_WINDOW;
+  if (sc.num_accelerators < 1) return CACE_E_ACCELERATORS;
+  // A negative unload delay can schedule a LoadComplete before the current
+  // event (time running backwards); the engine requires a monotone clock.
+  if (!(sc.unload_time_s >= 0.0) || !std::isfinite(sc.unload_time_s))
+    return CACE_E_INVALID | (1 << 8);
+  const int64_t n = L.off[sc.trace + 1] - L.off[sc.trace];
+  if (n == 0) return CACE_OK;
+  if (L.bad_model[sc.trace] >= 0) return CACE_E_RATES | (L.bad_model[sc.trace] << 8);
+  const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
+  if (cap < 1) return CACE_E_DEADLOCK;  // nothing can ever load (engine.cpp:235-237)
+  if (cap > kMaxLaneC) return CACE_E_INVALID | (2 << 8);
+  return CACE_OK;
+}
+
+inline std::string status_text(const HostCatalog& cat, int32_t status) {
+  const int code = status & 0xff;
+  const int m = status >> 8;
+  switch (code) {
+    case CACE_OK: return "";
+    case CACE_E_WINDOW: return "run: window_length must be >= 1";
+    case CACE_E_ACCELERATORS: return "run: need at least one accelerator";
+    case CACE_E_RATES: return "service_times: rates must be positive for " + model_name(cat.ids, m);
+    case CACE_E_CLOCK:
+      return "eviction_score: clock precedes last_used_s for " + model_name(cat.ids, m);
+    case CACE_E_DEADLOCK:
+      return "run: deadlock \xe2\x80\x94 pending requests with no schedulable event";
+    case CACE_E_RESIDENCY: return "run: residency bound violated";
+    default:
+      if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be finite and >= 0";
+      if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 16 is not supported by the lane kernel";
+      return "cace: invalid scenario (bad trace index or variant)";
+  }
+}
+
+}  // namespace cace

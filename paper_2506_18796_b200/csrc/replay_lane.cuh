@@ -29,55 +29,9 @@
 
 #include "../../include/cace_gpu.h"
 #include "glibc_log.cuh"
+#include "replay_types.h"
 
 namespace cace {
-
-enum : int { ST_IDLE = 0, ST_BUSY = 1, ST_LOADING = 2 };
-
-// One request in replay (sorted) order.  32 B = one sector: a lane advancing
-// its queue head fetches exactly one sector (two 128-bit loads).
-struct __align__(32) ReqRec {
-  double arrival;  // Request::arrival_time_s
-  double prefill;  // service_times(): prompt / prefill_rate   (engine.cpp:21-22)
-  double decode;   // service_times(): max(out,1) / decode_rate (engine.cpp:23-24)
-  uint32_t nxt;    // next sorted index with the same model (n if none)
-  uint32_t mc;     // model | task_class << 16
-};
-
-struct DevCatalog {
-  int M;
-  const double* load_time;  // [M] ModelDescriptor::load_time_s
-  const double* p2;         // [M] 1 / (1 + load_time / 100)  (policy.cpp:55)
-  const double* tokens;     // [M] (double) expected_output_tokens
-  const int* lex;           // [M] rank of model_id under std::string <
-};
-
-struct DumpDev {
-  const int32_t* slot;  // [n_scenarios] dump slot or -1; NULL = no dump
-  const int64_t* dump_off;  // [n_dump] offset of slot's per-request block
-  uint8_t* cold;
-  double *queue_wait, *load_wait, *prefill, *decode, *ttft, *e2e;
-  int64_t evict_cap;
-  int32_t* evict_model;
-  double* evict_clock;
-  int64_t* n_evict;
-};
-
-struct ReplayParams {
-  const ReqRec* rec;        // all traces, concatenated, sorted order
-  const int64_t* trace_off; // [T+1]
-  const uint32_t* first0;   // [T][M] first sorted index of each model
-  const uint32_t* perm;     // sorted index -> caller's request index
-  DevCatalog cat;
-  const double* log_tab;
-  const double* log_tab2;
-  int log_variant;
-  const cace_scenario_t* scen;
-  const int64_t* order;     // plan: scenario indices grouped by capacity
-  int64_t seg_begin, seg_end;
-  cace_summary_t* out;
-  DumpDev dump;
-};
 
 __device__ __forceinline__ uint64_t hmix(uint64_t h, uint64_t x) {
   h ^= x;
@@ -98,64 +52,42 @@ __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf,
   mc = q1.w;
 }
 
-// Per-lane replay state for one scenario.  Template C = capacity (slots):
-// the slot arrays live in registers with fully unrolled scans.
-template <int C>
-struct Lane {
-  // slots: model | state << 16, last_used, ServiceComplete time + push seq
-  int sms[C];
-  double slu[C], sdone[C];
-  uint32_t sseq[C];
-  int occ;
-  int ls;          // slot with the in-flight load (-1 none)
-  double lready;   // its LoadComplete time
-  uint32_t seqc;   // ServiceComplete push order
-  // queue head (first unserved request, replay order)
-  uint32_t head;
-  double ha, hpf, hdc, hlw;
-  uint32_t hnxt, hmc;
-  bool hc, hcold, harr;
-  double now;
-  // results
-  uint32_t hits, misses, evictions, loads, nc, nr;
-  double lo_sum, sttft, se2e, mttft, me2e;
-  uint64_t ho, he;
-  int status;
+// Slot word: model (bits 0-15) | lex rank of model_id (bits 18-31).
+__device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
+__device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
+
+// Event key (time, kind, seq) of engine.cpp:49-55; kind 0 LoadComplete,
+// 1 ServiceComplete, 2 Arrival.
+struct Cursor {
+  double t;
+  int kind;
+  uint32_t seq;
 };
 
-// Slot word: model (bits 0-15) | state (16-17) | lex rank of model_id (18-31).
-__device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
-__device__ __forceinline__ int slot_state(int v) { return (v >> 16) & 3; }
-__device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
-__device__ __forceinline__ int with_state(int v, int st) { return (v & ~(3 << 16)) | (st << 16); }
-
-// start_load (engine.cpp:123-132): the head's model into `target`.
-template <int C>
-__device__ __forceinline__ void start_load(Lane<C>& L, int target, double udelay, const double* s_lt,
-                                           const int* s_lex) {
-  const int hm = (int)(L.hmc & 0xffffu);
-  const double lt = s_lt[hm];
-  const double ready = (L.now + udelay) + lt;
-  L.hlw = ready - L.now;
-  L.lo_sum += lt;
-  ++L.loads;
-#pragma unroll
-  for (int s = 0; s < C; ++s)
-    if (s == target) {
-      L.sms[s] = hm | (ST_LOADING << 16) | (s_lex[hm] << 18);
-      L.slu[s] = L.now;
-    }
-  L.ls = target;
-  L.lready = ready;
+// key(ServiceComplete of a slot) <= cursor
+__device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
+  return d < c.t || (d == c.t && (c.kind > 1 || (c.kind == 1 && q <= c.seq)));
 }
 
-// Replays one scenario.  Two phases per iteration so the expensive part runs
-// converged across the warp:
-//   A (divergent, cheap): events + head-of-line dispatch (hits, service
-//     starts, free-slot loads) until the lane reaches an eviction decision
-//     or finishes;
-//   B (converged): the eviction decision — victim selection over the idle
-//     residents (policy.cpp:80-115) and the load that follows.
+// Replays one scenario = one reference run() (engine.cpp:76-239), REQUEST-
+// SYNCHRONOUSLY: iteration k of the loop processes request k (replay order)
+// from the moment it reaches the queue head to its service start.  This is
+// exact because, between two service starts, the reference's event loop can
+// only do the following (engine.cpp:157-230, policy.cpp:80-115):
+//   * queue empty -> the head's Arrival (a_k, 2, k) is the next relevant
+//     event; every ServiceComplete with key below it just idles its slot;
+//   * head resident & Idle -> served in the same dispatch (hit, case A);
+//   * head resident & Busy -> blocked until its own ServiceComplete; earlier
+//     completions only idle other slots (case B);
+//   * head not resident -> a free slot (case C), or an eviction decision at
+//     the current event if any slot is Idle (D1; forced when exactly one),
+//     or, if every slot is Busy, at the next ServiceComplete whose slot is
+//     then the only Idle one (forced victim, D2); then blocked until its
+//     LoadComplete (r, 0, .), before which completions only idle slots.
+// Completions are therefore applied in bulk against the event cursor, and
+// all lanes of a warp walk the same request index: the request record is a
+// warp-uniform broadcast load and divergence is confined to the case split.
+// Only D1 with >= 2 idle candidates evaluates eviction_score.
 // first/p4 are this lane's shared-memory columns (element m at [m*stride]).
 template <int C, bool DUMP>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* first,
@@ -172,6 +104,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
   const bool verbatim = sc.p1_mode == CACE_P1_VERBATIM;
   const uint32_t w = (uint32_t)sc.window_length;
   const double wd = (double)sc.window_length;
+  const double unload = sc.unload_time_s;
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -179,7 +112,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
   }
-
   if (need_win) {
     const uint32_t* f0 = P.first0 + (int64_t)sc.trace * M;
     for (int m = 0; m < M; ++m) first[m * stride] = __ldg(f0 + m);
@@ -190,342 +122,328 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
     for (int m = 0; m < M; ++m) p4tab[m * stride] = sc.w1 * (__ldg(P.cat.tokens + m) / norm);
   }
 
-  Lane<C> L;
+  // Slots (registers).  busy[s]: ServiceComplete pending at (sdone, sseq);
+  // otherwise Idle with last_used slu.  (Loading never outlives its own
+  // iteration.)
+  int sms[C];
+  double slu[C], sdone[C];
+  uint32_t sseq[C];
+  unsigned busy = 0;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
-    L.sms[s] = 0xffff;  // empty
-    L.slu[s] = 0.0;
-    L.sdone[s] = 0.0;
-    L.sseq[s] = 0;
+    sms[s] = 0xffff;
+    slu[s] = 0.0;
+    sdone[s] = 0.0;
+    sseq[s] = 0;
   }
-  L.occ = 0;
-  L.ls = -1;
-  L.lready = 0.0;
-  L.seqc = 0;
-  L.head = 0;
-  L.ha = L.hpf = L.hdc = L.hlw = 0.0;
-  L.hnxt = L.hmc = 0;
-  L.hc = L.hcold = L.harr = false;
-  L.now = 0.0;
-  L.hits = L.misses = L.evictions = L.loads = L.nc = L.nr = 0;
-  L.lo_sum = L.sttft = L.se2e = L.mttft = L.me2e = 0.0;
-  L.ho = L.he = CACE_HASH_SEED;
-  L.status = CACE_OK;
-  if (n > 0) load_rec(tr, L.ha, L.hpf, L.hdc, L.hnxt, L.hmc);
+  int occ = 0;
+  uint32_t seqc = 0;
+  Cursor cur{-INFINITY, 2, 0};
 
-  bool active = n > 0;
-  bool need_dec = false;
-  for (;;) {
-    // ================= phase A: cheap, divergent =================
-    while (active && !need_dec) {
-      // next completion: min (time, kind, seq) over the load and the busy
-      // slots (engine.cpp:49-55)
-      double tc = L.lready;
-      int sc_slot = L.ls;
-      bool cload = L.ls >= 0;
-      uint32_t qc = 0;
-#pragma unroll
-      for (int s = 0; s < C; ++s) {
-        const bool better = slot_state(L.sms[s]) == ST_BUSY &&
-                            (sc_slot < 0 || L.sdone[s] < tc ||
-                             (L.sdone[s] == tc && !cload && L.sseq[s] < qc));
-        if (better) {
-          tc = L.sdone[s];
-          sc_slot = s;
-          cload = false;
-          qc = L.sseq[s];
-        }
-      }
-      if (!L.harr && (sc_slot < 0 || L.ha < tc)) {
-        L.now = L.ha;  // arrival of the head into an empty queue
-        L.harr = true;
-      } else if (sc_slot < 0) {
-        L.status = CACE_E_DEADLOCK;  // pending requests, nothing schedulable
-        active = false;
-        break;
-      } else {
-        // Load/ServiceComplete: slot -> Idle, last_used = event time
-        // (engine.cpp:219-230)
-        L.now = tc;
-#pragma unroll
-        for (int s = 0; s < C; ++s)
-          if (s == sc_slot) {
-            L.sms[s] = with_state(L.sms[s], ST_IDLE);
-            L.slu[s] = tc;
-          }
-        if (cload) L.ls = -1;
-        if (!L.harr) continue;  // queue empty: dispatch has nothing to do
-      }
+  uint32_t hits = 0, evictions = 0, loads = 0, nc = 0, nr = 0;
+  double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
+  uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
-      // dispatch(now): head-of-line FIFO (engine.cpp:157-210)
-      for (;;) {
-        const int hm = (int)(L.hmc & 0xffffu);
-        int hs = -1, hst = ST_IDLE;
+  for (uint32_t k = 0; k < n; ++k) {
+    double a, pf, dc;
+    uint32_t nxt, mc;
+    load_rec(tr + k, a, pf, dc, nxt, mc);
+    const int m = (int)(mc & 0xffffu);
+
+    // Head not yet pending (j > previous head is pending iff a_j < now):
+    // advance to its Arrival event; completions with key below it idle
+    // their slots (engine.cpp:219-230).
+    if (!(a < cur.t)) {
 #pragma unroll
-        for (int s = 0; s < C; ++s)
-          if (slot_model(L.sms[s]) == hm) {
-            hs = s;
-            hst = slot_state(L.sms[s]);
-          }
-        if (!L.hc) {  // classify once (engine.cpp:163-173)
-          L.hc = true;
-          const bool hit = hs >= 0 && hst != ST_LOADING;
-          L.hits += hit ? 1u : 0u;
-          L.misses += hit ? 0u : 1u;
-          L.hcold = !hit;
+      for (int s = 0; s < C; ++s)
+        if ((busy >> s & 1u) && sdone[s] <= a) {
+          busy &= ~(1u << s);
+          slu[s] = sdone[s];
         }
-        if (hs >= 0) {
-          if (hst != ST_IDLE) break;  // busy or still loading
-          // start_service (engine.cpp:134-153)
-          const double qd = L.now - L.ha;
-          const double ttft = qd + L.hpf;
-          const double e2e = ttft + L.hdc;
-          const double done = (L.now + L.hpf) + L.hdc;
-#pragma unroll
-          for (int s = 0; s < C; ++s)
-            if (s == hs) {
-              L.sms[s] = with_state(L.sms[s], ST_BUSY);
-              L.sdone[s] = done;
-              L.sseq[s] = L.seqc;
-            }
-          ++L.seqc;
-          if ((L.hmc >> 16) == CACE_COMPLETION) {
-            ++L.nc;
-            L.sttft += ttft;
-            L.mttft = ttft > L.mttft ? ttft : L.mttft;
-          } else {
-            ++L.nr;
-            L.se2e += e2e;
-            L.me2e = e2e > L.me2e ? e2e : L.me2e;
-          }
-          L.ho = hmix(hmix(L.ho, dbits(ttft)), dbits(e2e) ^ (L.hcold ? 1ull : 0ull));
-          if (DUMP && dslot >= 0) {
-            const int64_t o = doff + P.perm[base + L.head];
-            if (P.dump.cold) P.dump.cold[o] = L.hcold ? 1 : 0;
-            if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - L.hlw;
-            if (P.dump.load_wait) P.dump.load_wait[o] = L.hlw;
-            if (P.dump.prefill) P.dump.prefill[o] = L.hpf;
-            if (P.dump.decode) P.dump.decode[o] = L.hdc;
-            if (P.dump.ttft) P.dump.ttft[o] = ttft;
-            if (P.dump.e2e) P.dump.e2e[o] = e2e;
-          }
-          // pop the head; the next is pending iff it arrived before now
-          if (need_win) first[hm * stride] = L.hnxt;
-          ++L.head;
-          if (L.head == n) {
-            active = false;
-            break;
-          }
-          load_rec(tr + L.head, L.ha, L.hpf, L.hdc, L.hnxt, L.hmc);
-          L.hc = false;
-          L.hcold = false;
-          L.hlw = 0.0;
-          L.harr = L.ha < L.now;
-          if (!L.harr) break;
-          continue;
-        }
-        if (L.occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
-          start_load(L, L.occ, 0.0, s_lt, s_lex);
-          ++L.occ;
-          break;
-        }
-        bool any_idle = false;
-#pragma unroll
-        for (int s = 0; s < C; ++s) any_idle |= slot_state(L.sms[s]) == ST_IDLE;
-        need_dec = any_idle;  // else every resident busy: wait (engine.cpp:203)
-        break;
-      }
+      cur = Cursor{a, 2, k};
     }
 
-    // ================= phase B: eviction decision, converged =================
-    if (need_dec) {
-      need_dec = false;
-      const double now = L.now;
-      // Sorted-first = min (last_used, lex) over idle residents = LRU victim.
-      int f = -1;
-      double flu = 0.0;
-      int flex = 0;
+    // classify (engine.cpp:163-173): resident and not Loading -> hit
+    int hs = -1;
 #pragma unroll
-      for (int s = 0; s < C; ++s) {
-        const int lx = slot_lex(L.sms[s]);
-        if (slot_state(L.sms[s]) == ST_IDLE &&
-            (f < 0 || L.slu[s] < flu || (L.slu[s] == flu && lx < flex))) {
-          f = s;
-          flu = L.slu[s];
-          flex = lx;
-        }
+    for (int s = 0; s < C; ++s)
+      if (slot_model(sms[s]) == m) hs = s;
+    double lw = 0.0;
+    const bool hit = hs >= 0;
+    if (hit) {
+      ++hits;
+      if (busy >> hs & 1u) {
+        // case B: wait for the model's own ServiceComplete
+        double td = 0.0;
+        uint32_t tq = 0;
+#pragma unroll
+        for (int s = 0; s < C; ++s)
+          if (s == hs) {
+            td = sdone[s];
+            tq = sseq[s];
+          }
+        cur = Cursor{td, 1, tq};
+#pragma unroll
+        for (int s = 0; s < C; ++s)
+          if ((busy >> s & 1u) && sc_le(sdone[s], sseq[s], cur)) {
+            busy &= ~(1u << s);
+            slu[s] = sdone[s];
+          }
       }
-      int victim = f;
-      if (!is_lru) {
-        // eviction_score for every idle entry (policy.cpp:39-78); the victim
-        // is the first strict max in sorted order.
-        uint32_t fm[C];
-        int rank[C];
+    } else {
+      int v;
+      double ud = 0.0;
+      if (occ < C) {  // case C: free slot, no unload delay (engine.cpp:184-187)
+        v = occ++;
+      } else {
+        const unsigned all = (1u << C) - 1u;
+        const unsigned idle = ~busy & all;
+        if (idle == 0) {
+          // D2: every resident busy; the next event is the min-key
+          // ServiceComplete, whose slot is then the only Idle one.
+          int s1 = -1;
+          double t1 = 0.0;
+          uint32_t q1 = 0;
 #pragma unroll
-        for (int s = 0; s < C; ++s) {
-          fm[s] = need_win ? first[slot_model(L.sms[s]) * stride] : 0u;
-          rank[s] = 0;
-        }
-        if (need_win) {
-          for (int mm = 0; mm < M; ++mm) {
-            const uint32_t x = first[mm * stride];
-#pragma unroll
-            for (int s = 0; s < C; ++s) rank[s] += x < fm[s] ? 1 : 0;
-          }
-        }
-        bool inwin[C];
-        bool bad_clock = false;
-#pragma unroll
-        for (int s = 0; s < C; ++s) {
-          bool iw = false;
-          if (variant != CACE_MINUS_P3) {
-            // in window [head, min(head + w, arrived)); fm >= head always
-            iw = fm[s] < n && fm[s] - L.head < w;
-            if (iw) iw = __ldg(&tr[fm[s]].arrival) < now;
-          }
-          inwin[s] = iw;
-          bad_clock |= slot_state(L.sms[s]) == ST_IDLE && now < L.slu[s];
-        }
-        // ---- screening pass in fp32 with a rigorous error bound: if one
-        // candidate's approximate total beats every other by more than the
-        // bound, it is the exact arg-max and the fp64 totals are not needed.
-        // |T~ - T| <= 2.6e-5 (3-ulp __logf on ln t < 70, Lipschitz-1 P1) plus
-        // fp32 rounding of the terms and sums (<= 2^-22 |T|); margin 2x that.
-        float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
-        int bs = -1;
-        bool exact = bad_clock;
-        const float wf = (float)sc.window_length;
-#pragma unroll
-        for (int s = 0; s < C; ++s) {
-          const int m = slot_model(L.sms[s]);
-          float p1 = 0.0f;
-          if (variant != CACE_MINUS_P1) {
-            const double d = now - L.slu[s];
-            const double t = d < 1.0 ? 1.0 : d;
-            exact |= !(t < 1e30);
-            const float p1v = __frcp_rn(1.0f + __logf((float)t));
-            p1 = verbatim ? p1v : 1.0f - p1v;
-          }
-          const float p2 = variant == CACE_MINUS_P2 ? 0.0f : (float)s_p2[m];
-          const float p3 =
-              variant == CACE_MINUS_P3 ? 0.0f : (inwin[s] ? __fdiv_rn((float)rank[s], wf) : 1.0f);
-          const float p4 = variant == CACE_MINUS_P4 ? 0.0f : (float)p4tab[m * stride];
-          const float T = ((p1 + p2) + p3) + p4;
-          if (slot_state(L.sms[s]) == ST_IDLE) {
-            tmax = fmaxf(tmax, fabsf(T));
-            exact |= !(fabsf(T) <= 1e6f);  // NaN / inf / huge: decide exactly
-            if (T > best) {
-              second = best;
-              best = T;
-              bs = s;
-            } else if (T > second) {
-              second = T;
+          for (int s = 0; s < C; ++s)
+            if (s1 < 0 || sdone[s] < t1 || (sdone[s] == t1 && sseq[s] < q1)) {
+              s1 = s;
+              t1 = sdone[s];
+              q1 = sseq[s];
             }
-          }
-        }
-        const float margin = 6e-5f + 4.8e-7f * tmax;
-        exact |= !(best - second > margin);
-        victim = bs;
-        if (exact) {
-          // ---- exact fp64 path (policy.cpp:39-115), bit-identical to the
-          // reference: needed for near-ties (3-11% of CACE decisions are
-          // exact ties broken by last_used, then model_id).
-          double tot[C];
-          int bad_lex = 1 << 30, bad_model = -1;
+          busy &= ~(1u << s1);
+          cur = Cursor{t1, 1, q1};
+          v = s1;
+        } else if ((idle & (idle - 1u)) == 0) {
+          v = __ffs(idle) - 1;  // exactly one candidate
+        } else {
+          // ---- D1: eviction decision among >= 2 idle residents --------
+          const double now = cur.t;
+          // Sorted-first = min (last_used, lex) over idle = the LRU victim.
+          int f = -1;
+          double flu = 0.0;
+          int flex = 0;
 #pragma unroll
           for (int s = 0; s < C; ++s) {
-            tot[s] = 0.0;
-            if (slot_state(L.sms[s]) != ST_IDLE) continue;
-            const int m = slot_model(L.sms[s]);
-            if (now < L.slu[s]) {  // eviction_score throws (policy.cpp:43-46)
-              const int lx = slot_lex(L.sms[s]);
-              if (lx < bad_lex) {
-                bad_lex = lx;
-                bad_model = m;
+            const int lx = slot_lex(sms[s]);
+            if ((idle >> s & 1u) && (f < 0 || slu[s] < flu || (slu[s] == flu && lx < flex))) {
+              f = s;
+              flu = slu[s];
+              flex = lx;
+            }
+          }
+          v = f;
+          if (!is_lru) {
+            uint32_t fm[C];
+            int rank[C];
+#pragma unroll
+            for (int s = 0; s < C; ++s) {
+              fm[s] = need_win ? first[slot_model(sms[s]) * stride] : 0u;
+              rank[s] = 0;
+            }
+            if (need_win) {
+              for (int mm = 0; mm < M; ++mm) {
+                const uint32_t x = first[mm * stride];
+#pragma unroll
+                for (int s = 0; s < C; ++s) rank[s] += x < fm[s] ? 1 : 0;
               }
             }
-            double p1 = 0.0;
-            if (variant != CACE_MINUS_P1) {
-              const double d = now - L.slu[s];
-              const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
-              const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
-              const double p1v = 1.0 / (1.0 + lg);
-              p1 = verbatim ? p1v : 1.0 - p1v;
-            }
-            const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[m];
-            const double p3 =
-                variant == CACE_MINUS_P3 ? 0.0 : (inwin[s] ? (double)rank[s] / wd : 1.0);
-            const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[m * stride];
-            tot[s] = ((p1 + p2) + p3) + p4;
-          }
-          if (bad_model >= 0) {
-            L.status = CACE_E_CLOCK | (bad_model << 8);
-            active = false;
-          } else {
-            victim = f;
-            double bt = 0.0;
+            bool inwin[C];
 #pragma unroll
-            for (int s = 0; s < C; ++s)
-              if (s == f) bt = tot[s];
-            if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
-              int blex = flex;
-              double blu = flu;
+            for (int s = 0; s < C; ++s) {
+              bool iw = false;
+              if (need_win) {
+                // window = [k, min(k + w, arrived)); resident idle models
+                // are not the head's, so fm > k
+                iw = fm[s] < n && fm[s] - k < w;
+                if (iw) iw = __ldg(&tr[fm[s]].arrival) < now;
+              }
+              inwin[s] = iw;
+            }
+            // Screening in fp32 with a rigorous bound: if one candidate's
+            // approximate total beats every other by more than the bound it
+            // is the exact arg-max.  |T~ - T| <= 2.6e-5 (3-ulp __logf on
+            // ln t < 70, Lipschitz-1 P1) plus fp32 rounding of terms and sums
+            // (<= 2^-22 |T|); the margin is twice that.
+            float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
+            int bs = -1;
+            bool exact = false;
+            const float wf = (float)sc.window_length;
+#pragma unroll
+            for (int s = 0; s < C; ++s) {
+              const int ms = slot_model(sms[s]);
+              float p1 = 0.0f;
+              if (variant != CACE_MINUS_P1) {
+                const double d = now - slu[s];
+                const double t = d < 1.0 ? 1.0 : d;
+                exact |= !(t < 1e30);
+                const float p1v = __frcp_rn(1.0f + __logf((float)t));
+                p1 = verbatim ? p1v : 1.0f - p1v;
+              }
+              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : (float)s_p2[ms];
+              const float p3 = variant == CACE_MINUS_P3
+                                   ? 0.0f
+                                   : (inwin[s] ? __fdiv_rn((float)rank[s], wf) : 1.0f);
+              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : (float)p4tab[ms * stride];
+              const float T = ((p1 + p2) + p3) + p4;
+              if (idle >> s & 1u) {
+                tmax = fmaxf(tmax, fabsf(T));
+                exact |= !(fabsf(T) <= 1e6f);  // NaN / inf / huge: decide exactly
+                if (T > best) {
+                  second = best;
+                  best = T;
+                  bs = s;
+                } else if (T > second) {
+                  second = T;
+                }
+              }
+            }
+            exact |= !(best - second > 6e-5f + 4.8e-7f * tmax);
+            v = bs;
+            if (exact) {
+              // Exact fp64 eviction_score (policy.cpp:39-78) and "first
+              // strict max in (last_used, model_id) order" (policy.cpp:92-113),
+              // bit-identical to the reference; used on near-ties (3-11% of
+              // CACE decisions are exact ties).
+              double tot[C];
 #pragma unroll
               for (int s = 0; s < C; ++s) {
-                const int lx = slot_lex(L.sms[s]);
-                const bool earlier = L.slu[s] < blu || (L.slu[s] == blu && lx < blex);
-                if (slot_state(L.sms[s]) == ST_IDLE && s != f &&
-                    (tot[s] > bt || (tot[s] == bt && earlier))) {
-                  victim = s;
-                  bt = tot[s];
-                  blu = L.slu[s];
-                  blex = lx;
+                tot[s] = 0.0;
+                if (!(idle >> s & 1u)) continue;
+                const int ms = slot_model(sms[s]);
+                double p1 = 0.0;
+                if (variant != CACE_MINUS_P1) {
+                  const double d = now - slu[s];
+                  const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
+                  const double lg =
+                      t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
+                  const double p1v = 1.0 / (1.0 + lg);
+                  p1 = verbatim ? p1v : 1.0 - p1v;
+                }
+                const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[ms];
+                const double p3 =
+                    variant == CACE_MINUS_P3 ? 0.0 : (inwin[s] ? (double)rank[s] / wd : 1.0);
+                const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[ms * stride];
+                tot[s] = ((p1 + p2) + p3) + p4;
+              }
+              v = f;
+              double bt = 0.0;
+#pragma unroll
+              for (int s = 0; s < C; ++s)
+                if (s == f) bt = tot[s];
+              if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
+                int blex = flex;
+                double blu = flu;
+#pragma unroll
+                for (int s = 0; s < C; ++s) {
+                  const int lx = slot_lex(sms[s]);
+                  const bool earlier = slu[s] < blu || (slu[s] == blu && lx < blex);
+                  if ((idle >> s & 1u) && s != f && (tot[s] > bt || (tot[s] == bt && earlier))) {
+                    v = s;
+                    bt = tot[s];
+                    blu = slu[s];
+                    blex = lx;
+                  }
                 }
               }
             }
           }
         }
-      }
-      if (active) {
-        int vm = -1;
+        // residents.erase(victim); evictions++ (engine.cpp:205-206)
+        int vm = 0;
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if (s == victim) vm = slot_model(L.sms[s]);
-        ++L.evictions;  // residents.erase(victim) (engine.cpp:205-206)
-        L.he = hmix(hmix(L.he, (uint64_t)vm), dbits(now));
+          if (s == v) vm = slot_model(sms[s]);
+        ++evictions;
+        he = hmix(hmix(he, (uint64_t)vm), dbits(cur.t));
         if (DUMP && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
-            if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = now;
+            if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = cur.t;
           }
           ++dn_ev;
         }
-        start_load(L, victim, sc.unload_time_s, s_lt, s_lex);
+        ud = unload;
       }
+      // start_load (engine.cpp:123-132), then blocked until LoadComplete
+      // (r, 0, .): completions strictly before r idle their slots.
+      const double lt = s_lt[m];
+      const double r = (cur.t + ud) + lt;
+      lw = r - cur.t;
+      lo_sum += lt;
+      ++loads;
+      const int word = m | (s_lex[m] << 18);
+#pragma unroll
+      for (int s = 0; s < C; ++s)
+        if (s == v) sms[s] = word;
+#pragma unroll
+      for (int s = 0; s < C; ++s)
+        if ((busy >> s & 1u) && sdone[s] < r) {
+          busy &= ~(1u << s);
+          slu[s] = sdone[s];
+        }
+      cur = Cursor{r, 0, 0};
+      hs = v;
     }
-    if (!active) break;
+
+    // start_service at now = cur.t (engine.cpp:134-153)
+    const double now = cur.t;
+    const double qd = now - a;
+    const double ttft = qd + pf;
+    const double e2e = ttft + dc;
+    const double done = (now + pf) + dc;
+#pragma unroll
+    for (int s = 0; s < C; ++s)
+      if (s == hs) {
+        sdone[s] = done;
+        sseq[s] = seqc;
+      }
+    busy |= 1u << hs;
+    ++seqc;
+    if ((mc >> 16) == CACE_COMPLETION) {
+      ++nc;
+      sttft += ttft;
+      mttft = ttft > mttft ? ttft : mttft;
+    } else {
+      ++nr;
+      se2e += e2e;
+      me2e = e2e > me2e ? e2e : me2e;
+    }
+    ho = hmix(hmix(ho, dbits(ttft)), dbits(e2e) ^ (hit ? 0ull : 1ull));
+    if (DUMP && dslot >= 0) {
+      const int64_t o = doff + P.perm[base + k];
+      if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
+      if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - lw;
+      if (P.dump.load_wait) P.dump.load_wait[o] = lw;
+      if (P.dump.prefill) P.dump.prefill[o] = pf;
+      if (P.dump.decode) P.dump.decode[o] = dc;
+      if (P.dump.ttft) P.dump.ttft[o] = ttft;
+      if (P.dump.e2e) P.dump.e2e[o] = e2e;
+    }
+    if (need_win) first[m * stride] = nxt;  // head leaves the window
   }
 
   cace_summary_t o;
-  o.hits = L.hits;
-  o.misses = L.misses;
-  o.evictions = L.evictions;
-  o.loads = L.loads;
-  o.load_overhead_s = L.lo_sum;
-  o.max_resident = L.occ;
-  o.status = L.status;
-  o.n_completion = L.nc;
-  o.n_reasoning = L.nr;
-  o.sum_ttft_completion = L.sttft;
-  o.sum_e2e_reasoning = L.se2e;
-  o.max_ttft_completion = L.mttft;
-  o.max_e2e_reasoning = L.me2e;
-  o.eviction_hash = L.he;
-  o.outcome_hash = L.ho;
+  o.hits = hits;
+  o.misses = n - hits;
+  o.evictions = evictions;
+  o.loads = loads;
+  o.load_overhead_s = lo_sum;
+  o.max_resident = occ;
+  o.status = CACE_OK;
+  o.n_completion = nc;
+  o.n_reasoning = nr;
+  o.sum_ttft_completion = sttft;
+  o.sum_e2e_reasoning = se2e;
+  o.max_ttft_completion = mttft;
+  o.max_e2e_reasoning = me2e;
+  o.eviction_hash = he;
+  o.outcome_hash = ho;
   P.out[sidx] = o;
   if (DUMP && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
 }
 
+#ifndef CACE_HOST_EMULATION
 // Block of LANE_BLOCK lanes; per-lane shared columns for first[] and p4[],
 // block-shared copy of the hot catalog columns.
 constexpr int LANE_BLOCK = 128;
@@ -554,5 +472,7 @@ __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P)
 inline size_t lane_smem_bytes(int M) {
   return (size_t)M * (8 + 8 + 4) + (size_t)M * LANE_BLOCK * (8 + 4);
 }
+
+#endif  // CACE_HOST_EMULATION
 
 }  // namespace cace

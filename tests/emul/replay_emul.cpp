@@ -1,0 +1,110 @@
+// TEST-ONLY host emulation of the replay kernel's device code.
+//
+// Compiles paper_2506_18796_b200/csrc/replay_lane.cuh's per-lane replay
+// (replay_scenario<C>) as ordinary host C++ by shimming the handful of CUDA
+// intrinsics it uses, so the engine's event algebra can be checked against
+// the reference oracle on a CPU-only box.  This library is never loaded by
+// the product (which has no CPU fallback); it exists only for tests/.
+#include <math.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#define CACE_HOST_EMULATION 1
+#define __device__
+#define __host__
+#define __global__
+#define __forceinline__ inline
+#define __launch_bounds__(...)
+struct uint4 { unsigned x, y, z, w; };
+template <typename T> static inline T __ldg(const T* p) { return *p; }
+static inline double __hiloint2double(int hi, int lo) {
+  uint64_t u = ((uint64_t)(uint32_t)hi << 32) | (uint32_t)lo;
+  double d;
+  std::memcpy(&d, &u, 8);
+  return d;
+}
+static inline long long __double_as_longlong(double d) { long long u; std::memcpy(&u, &d, 8); return u; }
+#define __logf(x) logf(x)
+static inline float __frcp_rn(float x) { return 1.0f / x; }
+static inline float __fdiv_rn(float a, float b) { return a / b; }
+static inline int __ffs(unsigned x) { return __builtin_ffs((int)x); }
+
+#include "../../paper_2506_18796_b200/csrc/replay_lane.cuh"
+#include "../../paper_2506_18796_b200/csrc/layout.hpp"
+
+using namespace cace;
+
+static const double kTab[256] = CACE_GLIBC_LOG_TAB;
+static const double kTab2[256] = CACE_GLIBC_LOG_TAB2;
+
+template <int C, bool D>
+static void one(const ReplayParams& P, int64_t i, std::vector<uint32_t>& first, std::vector<double>& p4,
+                const double* lt, const double* p2, const int* lex) {
+  replay_scenario<C, D>(P, i, first.data(), p4.data(), 1, lt, p2, lex);
+}
+
+extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                                     int32_t n_traces, const cace_scenario_t* sc, int64_t n,
+                                     cace_summary_t* out, int32_t log_variant,
+                                     const int32_t* dump_slot, const int64_t* dump_off,
+                                     uint8_t* cold, double* ttft, double* e2e, double* qw, double* lw,
+                                     int64_t evict_cap, int32_t* evict_model, double* evict_clock,
+                                     int64_t* n_evict) {
+  try {
+    HostCatalog cat;
+    cat.load(catalog);
+    HostLayout lay;
+    build_layout(cat, traces, n_traces, lay);
+    std::vector<int32_t> lex(cat.lex.begin(), cat.lex.end());
+    ReplayParams P{};
+    P.rec = lay.rec.data();
+    P.trace_off = lay.off.data();
+    P.first0 = lay.first0.data();
+    P.perm = lay.perm.data();
+    P.cat = DevCatalog{cat.M, cat.lt.data(), cat.p2.data(), cat.tok.data(), lex.data()};
+    P.log_tab = kTab;
+    P.log_tab2 = kTab2;
+    P.log_variant = log_variant;
+    P.scen = sc;
+    P.out = out;
+    P.dump.slot = dump_slot;
+    P.dump.dump_off = dump_off;
+    P.dump.cold = cold;
+    P.dump.ttft = ttft;
+    P.dump.e2e = e2e;
+    P.dump.queue_wait = qw;
+    P.dump.load_wait = lw;
+    P.dump.evict_cap = evict_cap;
+    P.dump.evict_model = evict_model;
+    P.dump.evict_clock = evict_clock;
+    P.dump.n_evict = n_evict;
+    std::vector<uint32_t> first(cat.M);
+    std::vector<double> p4(cat.M);
+    for (int64_t i = 0; i < n; ++i) {
+      const int32_t st = precheck(lay, sc[i]);
+      const int64_t len = (sc[i].trace >= 0 && sc[i].trace < lay.T) ? lay.off[sc[i].trace + 1] - lay.off[sc[i].trace] : 0;
+      if (st != CACE_OK || len == 0) {
+        std::memset(&out[i], 0, sizeof(cace_summary_t));
+        out[i].status = st;
+        out[i].eviction_hash = out[i].outcome_hash = CACE_HASH_SEED;
+        continue;
+      }
+      const int Cap = sc[i].num_accelerators * sc[i].models_per_accelerator;
+      const bool D = dump_slot != nullptr;
+      switch (Cap) {
+#define CASE(k) case k: D ? one<k, true>(P, i, first, p4, cat.lt.data(), cat.p2.data(), lex.data()) \
+                          : one<k, false>(P, i, first, p4, cat.lt.data(), cat.p2.data(), lex.data()); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+        default: return CACE_E_INVALID;
+      }
+    }
+    return 0;
+  } catch (const Invalid& e) {
+    return e.code;
+  }
+}
