@@ -239,14 +239,28 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     if (x.window_length != y.window_length) return x.window_length < y.window_length;
     return x.p1_mode < y.p1_mode;
   });
+  // Segments per capacity; inside, every (capacity, trace) group is padded
+  // to a whole number of warps with shadow lanes (copies of the group's
+  // first scenario that write nothing) so each warp is trace-uniform and can
+  // walk its trace in lockstep.
+  std::vector<int64_t> order;
+  order.reserve(ok.size() + 32 * 64);
   for (size_t k = 0; k < ok.size();) {
     const int C = capof(ok[k]);
+    const int64_t seg_b = (int64_t)order.size();
     size_t j = k;
-    while (j < ok.size() && capof(ok[j]) == C) ++j;
-    e->segs.push_back({C, (int64_t)k, (int64_t)j});
+    while (j < ok.size() && capof(ok[j]) == C) {
+      const int t = sc[ok[j]].trace;
+      size_t g = j;
+      while (g < ok.size() && capof(ok[g]) == C && sc[ok[g]].trace == t) order.push_back(ok[g++]);
+      const int64_t pad = (32 - (int64_t)(g - j) % 32) % 32;
+      for (int64_t q = 0; q < pad; ++q) order.push_back(ok[j] | (int64_t)kShadowBit);
+      j = g;
+    }
+    e->segs.push_back({C, seg_b, (int64_t)order.size()});
     k = j;
   }
-  e->d_order.upload(ok.data(), ok.size(), e->stream);
+  e->d_order.upload(order.data(), order.size(), e->stream);
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
   e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);
   CK(cudaStreamSynchronize(e->stream));

@@ -18,9 +18,9 @@
 //     j > head counts as arrived at event time `now` iff a[j] < now.
 //   * The pending queue is the contiguous sorted range [head, arrived), so
 //     the lookahead window is [head, min(head + w, arrived)) and needs no
-//     storage: first[m] (first index >= head requesting model m) is kept per
-//     lane in shared memory and rank(m) = #{m' : first[m'] < first[m]}
-//     (dedup_window, policy.cpp:22-37).
+//     storage beyond first[m] (first index >= head requesting model m) and
+//     rank(m) = #{m' : first[m'] < first[m]} (dedup_window,
+//     policy.cpp:22-37), kept once per warp (see Window).
 //   * All fp64 arithmetic uses the reference's operation order with no
 //     contraction (built with -fmad=false); P1's log is the glibc
 //     restatement (glibc_log.cuh).
@@ -69,6 +69,72 @@ __device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
   return d < c.t || (d == c.t && (c.kind > 1 || (c.kind == 1 && q <= c.seq)));
 }
 
+// Lookahead-window state (dedup_window, policy.cpp:22-37) for the warp.
+// Because every lane of a warp replays the same trace in lockstep (the plan
+// makes warps trace-uniform), first[m] — the first replay index >= the
+// current head that requests model m — and rank[m] = #{m' : first[m'] <
+// first[m]} are identical across the warp, so they live once per warp in
+// shared memory.  When the head k (model mk) is served, mk's first moves to
+// nxt[k]; every model whose first lies before nxt loses mk from its
+// "before" set, and mk's new rank is the ballot count of those models.
+struct Window {
+  uint32_t* first;  // [M]
+  uint32_t* rank;   // [M]
+  int M;
+};
+
+__device__ __forceinline__ void window_init(const Window& W, const uint32_t* f0) {
+#ifdef CACE_HOST_EMULATION
+  for (int m = 0; m < W.M; ++m) W.first[m] = f0[m];
+  for (int m = 0; m < W.M; ++m) {
+    uint32_t r = 0;
+    for (int q = 0; q < W.M; ++q) r += f0[q] < f0[m] ? 1u : 0u;
+    W.rank[m] = r;
+  }
+#else
+  const int lane = threadIdx.x & 31;
+  for (int m = lane; m < W.M; m += 32) W.first[m] = __ldg(f0 + m);
+  __syncwarp();
+  for (int m = lane; m < W.M; m += 32) {
+    const uint32_t fm = W.first[m];
+    uint32_t r = 0;
+    for (int q = 0; q < W.M; ++q) r += W.first[q] < fm ? 1u : 0u;
+    W.rank[m] = r;
+  }
+  __syncwarp();
+#endif
+}
+
+// Head k with model mk leaves the window; its next occurrence is nx.
+__device__ __forceinline__ void window_advance(const Window& W, int mk, uint32_t nx) {
+#ifdef CACE_HOST_EMULATION
+  uint32_t cnt = 0;
+  for (int j = 0; j < W.M; ++j)
+    if (j != mk && W.first[j] < nx) {
+      W.rank[j] -= 1;
+      ++cnt;
+    }
+  W.first[mk] = nx;
+  W.rank[mk] = cnt;
+#else
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  uint32_t cnt = 0;
+  for (int base = 0; base < W.M; base += 32) {
+    const int j = base + lane;
+    const bool before = j < W.M && j != mk && W.first[j] < nx;
+    cnt += __popc(__ballot_sync(0xffffffffu, before));
+    if (before) W.rank[j] -= 1;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    W.first[mk] = nx;
+    W.rank[mk] = cnt;
+  }
+  __syncwarp();
+#endif
+}
+
 // Replays one scenario = one reference run() (engine.cpp:76-239), REQUEST-
 // SYNCHRONOUSLY: iteration k of the loop processes request k (replay order)
 // from the moment it reaches the queue head to its service start.  This is
@@ -90,9 +156,10 @@ __device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
 // Only D1 with >= 2 idle candidates evaluates eviction_score.
 // first/p4 are this lane's shared-memory columns (element m at [m*stride]).
 template <int C, bool DUMP>
-__device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* first,
-                                double* p4tab, int stride, const double* s_lt,
-                                const double* s_p2, const int* s_lex) {
+__device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, const Window& W,
+                                bool warp_win, double* p4tab, float* p4f, int stride,
+                                const double* s_lt, const double* s_p2, const float* s_p2f,
+                                const int* s_lex) {
   const cace_scenario_t sc = P.scen[sidx];
   const int M = P.cat.M;
   const int64_t base = P.trace_off[sc.trace];
@@ -106,20 +173,23 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
   const double wd = (double)sc.window_length;
   const double unload = sc.unload_time_s;
 
+  const float rcpw = 1.0f / (float)sc.window_length;
+
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
-  if (DUMP) {
+  if (DUMP && !shadow) {
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
   }
-  if (need_win) {
-    const uint32_t* f0 = P.first0 + (int64_t)sc.trace * M;
-    for (int m = 0; m < M; ++m) first[m * stride] = __ldg(f0 + m);
-  }
+  if (warp_win) window_init(W, P.first0 + (int64_t)sc.trace * M);
   if (!is_lru) {
-    // p4 = w1 * (tokens / normalizer)   (policy.cpp:66-67)
+    // p4 = w1 * (tokens / normalizer)   (policy.cpp:66-67); fp32 copy for screening
     const double norm = (double)sc.output_token_normalizer;
-    for (int m = 0; m < M; ++m) p4tab[m * stride] = sc.w1 * (__ldg(P.cat.tokens + m) / norm);
+    for (int m = 0; m < M; ++m) {
+      const double p4 = sc.w1 * (__ldg(P.cat.tokens + m) / norm);
+      p4tab[m * stride] = p4;
+      p4f[m * stride] = (float)p4;
+    }
   }
 
   // Slots (registers).  busy[s]: ServiceComplete pending at (sdone, sseq);
@@ -144,10 +214,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
   double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
   uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
+  // Software-pipelined record stream: request k+1 is fetched while k is
+  // processed (the record is a warp-uniform broadcast load).
+  double na = 0.0, npf = 0.0, ndc = 0.0;
+  uint32_t nnxt = 0, nmc = 0;
+  if (n > 0) load_rec(tr, na, npf, ndc, nnxt, nmc);
   for (uint32_t k = 0; k < n; ++k) {
-    double a, pf, dc;
-    uint32_t nxt, mc;
-    load_rec(tr + k, a, pf, dc, nxt, mc);
+    const double a = na, pf = npf, dc = ndc;
+    const uint32_t nxt = nnxt, mc = nmc;
+    if (k + 1 < n) load_rec(tr + k + 1, na, npf, ndc, nnxt, nmc);
     const int m = (int)(mc & 0xffffu);
 
     // Head not yet pending (j > previous head is pending iff a_j < now):
@@ -234,41 +309,32 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
           }
           v = f;
           if (!is_lru) {
-            uint32_t fm[C];
-            int rank[C];
+            // Window position of each slot's model: p3 = rank / w when its
+            // first pending occurrence lies in [k, min(k + w, arrived)),
+            // else 1 (policy.cpp:57-64).  Resident idle models are not the
+            // head's, so first > k.  pos[s] = rank, or -1 when outside.
+            int pos[C];
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              fm[s] = need_win ? first[slot_model(sms[s]) * stride] : 0u;
-              rank[s] = 0;
-            }
-            if (need_win) {
-              for (int mm = 0; mm < M; ++mm) {
-                const uint32_t x = first[mm * stride];
-#pragma unroll
-                for (int s = 0; s < C; ++s) rank[s] += x < fm[s] ? 1 : 0;
-              }
-            }
-            bool inwin[C];
-#pragma unroll
-            for (int s = 0; s < C; ++s) {
-              bool iw = false;
+              pos[s] = -1;
               if (need_win) {
-                // window = [k, min(k + w, arrived)); resident idle models
-                // are not the head's, so fm > k
-                iw = fm[s] < n && fm[s] - k < w;
-                if (iw) iw = __ldg(&tr[fm[s]].arrival) < now;
+                const int ms = slot_model(sms[s]);
+                const uint32_t fmv = W.first[ms];
+                bool iw = fmv < n && fmv - k < w;
+                if (iw) iw = __ldg(&tr[fmv].arrival) < now;
+                if (iw) pos[s] = (int)W.rank[ms];
               }
-              inwin[s] = iw;
             }
             // Screening in fp32 with a rigorous bound: if one candidate's
             // approximate total beats every other by more than the bound it
-            // is the exact arg-max.  |T~ - T| <= 2.6e-5 (3-ulp __logf on
-            // ln t < 70, Lipschitz-1 P1) plus fp32 rounding of terms and sums
-            // (<= 2^-22 |T|); the margin is twice that.
+            // is the exact arg-max.  Error of the fp32 total: |dL| <= 2.3e-5
+            // (3-ulp __logf, ln t < 70) propagates with Lipschitz constant 1
+            // through 1/(1+L); __fdividef / the rank*(1/w) product / the
+            // term conversions and three fp32 sums add <= 2^-21 (|T| + 4).
+            // The margin is twice the worst case.
             float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
             int bs = -1;
             bool exact = false;
-            const float wf = (float)sc.window_length;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
               const int ms = slot_model(sms[s]);
@@ -277,14 +343,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
                 const double d = now - slu[s];
                 const double t = d < 1.0 ? 1.0 : d;
                 exact |= !(t < 1e30);
-                const float p1v = __frcp_rn(1.0f + __logf((float)t));
+                const float p1v = __fdividef(1.0f, 1.0f + __logf((float)t));
                 p1 = verbatim ? p1v : 1.0f - p1v;
               }
-              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : (float)s_p2[ms];
-              const float p3 = variant == CACE_MINUS_P3
-                                   ? 0.0f
-                                   : (inwin[s] ? __fdiv_rn((float)rank[s], wf) : 1.0f);
-              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : (float)p4tab[ms * stride];
+              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : s_p2f[ms];
+              const float p3 =
+                  variant == CACE_MINUS_P3 ? 0.0f : (pos[s] >= 0 ? (float)pos[s] * rcpw : 1.0f);
+              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : p4f[ms * stride];
               const float T = ((p1 + p2) + p3) + p4;
               if (idle >> s & 1u) {
                 tmax = fmaxf(tmax, fabsf(T));
@@ -298,7 +363,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
                 }
               }
             }
-            exact |= !(best - second > 6e-5f + 4.8e-7f * tmax);
+            exact |= !(best - second > 6e-5f + 1e-6f * (tmax + 4.0f));
             v = bs;
             if (exact) {
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
@@ -322,7 +387,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
                 }
                 const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[ms];
                 const double p3 =
-                    variant == CACE_MINUS_P3 ? 0.0 : (inwin[s] ? (double)rank[s] / wd : 1.0);
+                    variant == CACE_MINUS_P3 ? 0.0 : (pos[s] >= 0 ? (double)pos[s] / wd : 1.0);
                 const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[ms * stride];
                 tot[s] = ((p1 + p2) + p3) + p4;
               }
@@ -420,7 +485,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
       if (P.dump.ttft) P.dump.ttft[o] = ttft;
       if (P.dump.e2e) P.dump.e2e[o] = e2e;
     }
-    if (need_win) first[m * stride] = nxt;  // head leaves the window
+    if (warp_win) window_advance(W, m, nxt);  // head leaves the window
   }
 
   cace_summary_t o;
@@ -439,14 +504,17 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, uint32_t* f
   o.max_e2e_reasoning = me2e;
   o.eviction_hash = he;
   o.outcome_hash = ho;
+  if (shadow) return;  // warp padding lane: replayed for lockstep, no output
   P.out[sidx] = o;
   if (DUMP && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
 }
 
 #ifndef CACE_HOST_EMULATION
-// Block of LANE_BLOCK lanes; per-lane shared columns for first[] and p4[],
-// block-shared copy of the hot catalog columns.
+// Block of LANE_BLOCK lanes (4 trace-uniform warps).  Shared memory:
+// block-shared hot catalog columns, per-lane p4 columns (fp64 exact + fp32
+// screening copy), per-warp lookahead window (first/rank).
 constexpr int LANE_BLOCK = 128;
+constexpr uint64_t kShadowBit = 1ull << 62;  // plan entry = warp padding lane
 
 template <int C, bool DUMP>
 __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P) {
@@ -454,23 +522,36 @@ __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P)
   const int M = P.cat.M;
   double* s_lt = reinterpret_cast<double*>(smem);
   double* s_p2 = s_lt + M;
-  double* p4tab = s_p2 + M;                                      // [M][LANE_BLOCK]
-  int* s_lex = reinterpret_cast<int*>(p4tab + (size_t)M * LANE_BLOCK);
-  uint32_t* first = reinterpret_cast<uint32_t*>(s_lex + M);       // [M][LANE_BLOCK]
+  double* p4tab = s_p2 + M;                                          // [M][LANE_BLOCK]
+  float* s_p2f = reinterpret_cast<float*>(p4tab + (size_t)M * LANE_BLOCK);
+  float* p4f = s_p2f + M;                                            // [M][LANE_BLOCK]
+  int* s_lex = reinterpret_cast<int*>(p4f + (size_t)M * LANE_BLOCK);
+  uint32_t* wfirst = reinterpret_cast<uint32_t*>(s_lex + M);         // [4][M]
+  uint32_t* wrank = wfirst + (size_t)(LANE_BLOCK / 32) * M;          // [4][M]
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
+    s_p2f[m] = (float)P.cat.p2[m];
     s_lex[m] = P.cat.lex[m];
   }
   __syncthreads();
   const int64_t gi = P.seg_begin + (int64_t)blockIdx.x * LANE_BLOCK + threadIdx.x;
-  if (gi >= P.seg_end) return;
-  replay_scenario<C, DUMP>(P, P.order[gi], first + threadIdx.x, p4tab + threadIdx.x, LANE_BLOCK,
-                           s_lt, s_p2, s_lex);
+  if (gi >= P.seg_end) return;  // the plan pads groups to whole warps
+  const uint64_t e = (uint64_t)P.order[gi];
+  const bool shadow = (e & kShadowBit) != 0;
+  const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
+  const int variant = P.scen[sidx].variant;
+  const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
+  const bool warp_win = __any_sync(0xffffffffu, need_win);
+  const int warp = threadIdx.x >> 5;
+  const Window W{wfirst + (size_t)warp * M, wrank + (size_t)warp * M, M};
+  replay_scenario<C, DUMP>(P, sidx, shadow, W, warp_win, p4tab + threadIdx.x, p4f + threadIdx.x,
+                           LANE_BLOCK, s_lt, s_p2, s_p2f, s_lex);
 }
 
 inline size_t lane_smem_bytes(int M) {
-  return (size_t)M * (8 + 8 + 4) + (size_t)M * LANE_BLOCK * (8 + 4);
+  return (size_t)M * (8 + 8 + 4 + 4) + (size_t)M * LANE_BLOCK * (8 + 4) +
+         (size_t)(LANE_BLOCK / 32) * M * 8;
 }
 
 #endif  // CACE_HOST_EMULATION
