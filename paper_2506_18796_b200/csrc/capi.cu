@@ -215,7 +215,8 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   std::vector<int64_t> ok;
   ok.reserve(n);
   for (int64_t i = 0; i < n; ++i) {
-    const int32_t st = precheck(e->lay, sc[i]);
+    int32_t st = precheck(e->lay, sc[i]);
+    if (st == CACE_OK) st = precheck_pool(e->cat.M);
     const bool tv = sc[i].trace >= 0 && sc[i].trace < e->lay.T;
     const int64_t len = tv ? e->lay.off[sc[i].trace + 1] - e->lay.off[sc[i].trace] : 0;
     if (st != CACE_OK || len == 0) {
@@ -267,26 +268,32 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C, bool DUMP>
+template <int C, int MW, bool DUMP>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(replay_lane_kernel<C, DUMP>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
-  replay_lane_kernel<C, DUMP><<<grid, LANE_BLOCK, smem, s>>>(P);
+  replay_lane_kernel<C, MW, DUMP><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 
-template <bool DUMP>
-void dispatch_lane(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+template <int MW, bool DUMP>
+void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   switch (C) {
 #define CASE(k) \
-  case k: launch_lane<k, DUMP>(P, count, smem, s); break;
+  case k: launch_lane<k, MW, DUMP>(P, count, smem, s); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
     default: throw Invalid{CACE_E_INVALID, "cace: capacity not supported by the lane kernel"};
   }
+}
+
+void dispatch_lane(bool dump, int C, const ReplayParams& P, int64_t count, size_t smem,
+                   cudaStream_t s) {
+  const bool mw1 = P.cat.M <= 32;
+  if (dump)
+    mw1 ? dispatch_lane_c<1, true>(C, P, count, smem, s) : dispatch_lane_c<2, true>(C, P, count, smem, s);
+  else
+    mw1 ? dispatch_lane_c<1, false>(C, P, count, smem, s) : dispatch_lane_c<2, false>(C, P, count, smem, s);
 }
 
 void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary_t* d_out,
@@ -321,10 +328,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
       const auto& g = e->segs[k];
       P.seg_begin = g.b;
       P.seg_end = g.e;
-      if (dump_on)
-        dispatch_lane<true>(g.C, P, g.e - g.b, smem, ws);
-      else
-        dispatch_lane<false>(g.C, P, g.e - g.b, smem, ws);
+      dispatch_lane(dump_on, g.C, P, g.e - g.b, smem, ws);
       ++e->last_launches;
     }
     if (nseg > 1)

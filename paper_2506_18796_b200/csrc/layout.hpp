@@ -161,6 +161,9 @@ inline int32_t precheck(const HostLayout& L, const cace_scenario_t& sc) {
   return CACE_OK;
 }
 
+// Model pools beyond the lane kernel's register window (64 models).
+inline int32_t precheck_pool(int M) { return M > 64 ? (CACE_E_INVALID | (3 << 8)) : CACE_OK; }
+
 inline std::string status_text(const HostCatalog& cat, int32_t status) {
   const int code = status & 0xff;
   const int m = status >> 8;
@@ -177,6 +180,7 @@ inline std::string status_text(const HostCatalog& cat, int32_t status) {
     default:
       if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be finite and >= 0";
       if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 16 is not supported by the lane kernel";
+      if (code == CACE_E_INVALID && m == 3) return "cace: model pools > 64 are not supported by the lane kernel";
       return "cace: invalid scenario (bad trace index or variant)";
   }
 }

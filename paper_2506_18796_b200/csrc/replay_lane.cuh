@@ -1,30 +1,48 @@
-// Lane-per-scenario trace-replay kernel (sm_100a).
+// Lane-per-scenario, request-synchronous trace-replay kernel (sm_100a).
 //
 // One thread replays one scenario = one reference run(trace, catalog,
-// cluster, policy) (engine.cpp:76-239 + policy.cpp:22-115), bit-exact.
-// Lanes of a warp replay scenarios of the same trace and capacity (the host
-// plan groups them), so they read the same request records; the trace is
-// L2-resident and each request record is one 32-B sector.
+// cluster, policy) (engine.cpp:76-239 + policy.cpp:22-115), bit-exact.  The
+// host plan makes every warp trace-uniform (capacity/trace groups padded to
+// whole warps with shadow lanes), and the replay loop is organised so that
+// iteration k of EVERY lane processes request k of the trace — the request
+// record is a warp-uniform broadcast load and the lanes never drift apart.
 //
-// Event model (exactly the reference's min-heap order (time, kind, seq),
-// engine.cpp:49-55, without a heap):
-//   * at most ONE LoadComplete is ever in flight (only the queue head starts
-//     loads and it stays head until served), kind 0;
-//   * one ServiceComplete per Busy slot, kind 1, seq = service-start order;
-//   * Arrivals, kind 2, in (time, index) order.  An Arrival into a non-empty
-//     queue cannot change any dispatch decision (the head was already
-//     examined and nothing it waits on changed), so only the arrival of the
-//     head into an EMPTY queue is processed as an event; every other request
-//     j > head counts as arrived at event time `now` iff a[j] < now.
-//   * The pending queue is the contiguous sorted range [head, arrived), so
-//     the lookahead window is [head, min(head + w, arrived)) and needs no
-//     storage beyond first[m] (first index >= head requesting model m) and
-//     rank(m) = #{m' : first[m'] < first[m]} (dedup_window,
-//     policy.cpp:22-37), kept once per warp (see Window).
-//   * All fp64 arithmetic uses the reference's operation order with no
-//     contraction (built with -fmad=false); P1's log is the glibc
-//     restatement (glibc_log.cuh).
+// Why request k can be processed in one step (the reference's min-heap order
+// (time, kind, seq) of engine.cpp:49-55; kind 0 LoadComplete, 1
+// ServiceComplete, 2 Arrival).  Between two service starts the reference's
+// event loop can only do the following (engine.cpp:157-230,
+// policy.cpp:80-115):
+//   * queue empty -> the head's Arrival (a_k, 2, k) is the next relevant
+//     event; each ServiceComplete with a smaller key just idles its slot
+//     (last_used = its time) — dispatch with an empty queue does nothing;
+//   * head resident & Idle -> served in the current dispatch (a hit);
+//   * head resident & Busy -> blocked until its own ServiceComplete; earlier
+//     completions only idle other slots (the head blocks the FIFO);
+//   * head not resident -> a free slot (load without unload delay), or an
+//     eviction decision at the current event if any slot is Idle (forced
+//     when exactly one), or, if every slot is Busy, at the next
+//     ServiceComplete, whose slot is then the only Idle one (forced victim);
+//     then blocked until its LoadComplete (r, 0, .), before which
+//     completions only idle slots.  At most one load is ever in flight.
+//   * An Arrival into a non-empty queue never changes a decision; request
+//     j > head is pending at event time `now` iff a_j < now.
+// So completions are applied in bulk against the event cursor, the pending
+// queue is the contiguous range [k, arrived), and only a decision with >= 2
+// idle candidates evaluates eviction_score.
+//
+// Lookahead window (dedup_window, policy.cpp:22-37): p3 of a resident model
+// m needs first[m] (first replay index >= k requesting m) and rank(m) =
+// #{m' : first[m'] < first[m]}.  Both depend only on the trace and k, so they
+// are warp-wide state held in registers distributed over the lanes (lane j
+// owns models j, j+32, ...); they are gathered with shuffles when some lane
+// of the warp faces a decision and advanced with one ballot/popc per request.
+//
+// All fp64 arithmetic uses the reference's operation order with no
+// contraction (built with -fmad=false); P1's log is the glibc restatement
+// (glibc_log.cuh).  Decisions are first screened in fp32 with a rigorous
+// error margin; near-ties fall back to the exact fp64 scores.
 #pragma once
+#include <math.h>
 #include <stdint.h>
 
 #include "../../include/cace_gpu.h"
@@ -56,8 +74,7 @@ __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf,
 __device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
 __device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
 
-// Event key (time, kind, seq) of engine.cpp:49-55; kind 0 LoadComplete,
-// 1 ServiceComplete, 2 Arrival.
+// Event key (time, kind, seq) of engine.cpp:49-55.
 struct Cursor {
   double t;
   int kind;
@@ -69,97 +86,112 @@ __device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
   return d < c.t || (d == c.t && (c.kind > 1 || (c.kind == 1 && q <= c.seq)));
 }
 
-// Lookahead-window state (dedup_window, policy.cpp:22-37) for the warp.
-// Because every lane of a warp replays the same trace in lockstep (the plan
-// makes warps trace-uniform), first[m] — the first replay index >= the
-// current head that requests model m — and rank[m] = #{m' : first[m'] <
-// first[m]} are identical across the warp, so they live once per warp in
-// shared memory.  When the head k (model mk) is served, mk's first moves to
-// nxt[k]; every model whose first lies before nxt loses mk from its
-// "before" set, and mk's new rank is the ballot count of those models.
-struct Window {
-  uint32_t* first;  // [M]
-  uint32_t* rank;   // [M]
+constexpr unsigned kFull = 0xffffffffu;
+
+// Warp-wide lookahead window (see the file comment).  MW registers per lane:
+// lane j owns models j + 32q, q < MW.
+template <int MW>
+struct RegWindow {
+#ifdef CACE_HOST_EMULATION
+  uint32_t f[32 * MW], r[32 * MW];
   int M;
+  void init(const uint32_t* f0, int M_) {
+    M = M_;
+    for (int m = 0; m < M; ++m) f[m] = f0[m];
+    for (int m = 0; m < M; ++m) {
+      uint32_t c = 0;
+      for (int q = 0; q < M; ++q) c += f0[q] < f0[m] ? 1u : 0u;
+      r[m] = c;
+    }
+  }
+  void gather(int ms, uint32_t& fm, uint32_t& rk) const {
+    fm = ms < M ? f[ms] : 0xffffffffu;
+    rk = ms < M ? r[ms] : 0u;
+  }
+  void advance(int mk, uint32_t nx) {
+    uint32_t cnt = 0;
+    for (int j = 0; j < M; ++j)
+      if (j != mk && f[j] < nx) {
+        r[j] -= 1;
+        ++cnt;
+      }
+    f[mk] = nx;
+    r[mk] = cnt;
+  }
+#else
+  uint32_t f[MW], r[MW];
+  int M;
+  __device__ __forceinline__ void init(const uint32_t* f0, int M_) {
+    M = M_;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < MW; ++q) {
+      const int m = lane + 32 * q;
+      f[q] = m < M ? __ldg(f0 + m) : 0xffffffffu;
+      uint32_t c = 0;
+      for (int mm = 0; mm < M; ++mm) c += __ldg(f0 + mm) < f[q] ? 1u : 0u;
+      r[q] = c;
+    }
+  }
+  // Collective (all 32 lanes): this lane reads model ms's (first, rank).
+  __device__ __forceinline__ void gather(int ms, uint32_t& fm, uint32_t& rk) const {
+    const int src = ms & 31, qq = ms >> 5;
+    fm = 0xffffffffu;
+    rk = 0u;
+#pragma unroll
+    for (int q = 0; q < MW; ++q) {
+      const uint32_t a = __shfl_sync(kFull, f[q], src);
+      const uint32_t b = __shfl_sync(kFull, r[q], src);
+      if (q == qq) {
+        fm = a;
+        rk = b;
+      }
+    }
+  }
+  // Collective: the head (model mk) is served; mk's first becomes nx.
+  __device__ __forceinline__ void advance(int mk, uint32_t nx) {
+    const int lane = threadIdx.x & 31;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < MW; ++q) {
+      const int m = lane + 32 * q;
+      const bool before = m < M && m != mk && f[q] < nx;
+      cnt += __popc(__ballot_sync(kFull, before));
+      if (before) r[q] -= 1;
+    }
+#pragma unroll
+    for (int q = 0; q < MW; ++q)
+      if (lane + 32 * q == mk) {
+        f[q] = nx;
+        r[q] = cnt;
+      }
+  }
+#endif
 };
 
-__device__ __forceinline__ void window_init(const Window& W, const uint32_t* f0) {
+__device__ __forceinline__ bool warp_any(bool p) {
 #ifdef CACE_HOST_EMULATION
-  for (int m = 0; m < W.M; ++m) W.first[m] = f0[m];
-  for (int m = 0; m < W.M; ++m) {
-    uint32_t r = 0;
-    for (int q = 0; q < W.M; ++q) r += f0[q] < f0[m] ? 1u : 0u;
-    W.rank[m] = r;
-  }
+  return p;
 #else
-  const int lane = threadIdx.x & 31;
-  for (int m = lane; m < W.M; m += 32) W.first[m] = __ldg(f0 + m);
-  __syncwarp();
-  for (int m = lane; m < W.M; m += 32) {
-    const uint32_t fm = W.first[m];
-    uint32_t r = 0;
-    for (int q = 0; q < W.M; ++q) r += W.first[q] < fm ? 1u : 0u;
-    W.rank[m] = r;
-  }
-  __syncwarp();
+  return __any_sync(kFull, p);
 #endif
 }
 
-// Head k with model mk leaves the window; its next occurrence is nx.
-__device__ __forceinline__ void window_advance(const Window& W, int mk, uint32_t nx) {
-#ifdef CACE_HOST_EMULATION
-  uint32_t cnt = 0;
-  for (int j = 0; j < W.M; ++j)
-    if (j != mk && W.first[j] < nx) {
-      W.rank[j] -= 1;
-      ++cnt;
-    }
-  W.first[mk] = nx;
-  W.rank[mk] = cnt;
-#else
-  const int lane = threadIdx.x & 31;
-  __syncwarp();
-  uint32_t cnt = 0;
-  for (int base = 0; base < W.M; base += 32) {
-    const int j = base + lane;
-    const bool before = j < W.M && j != mk && W.first[j] < nx;
-    cnt += __popc(__ballot_sync(0xffffffffu, before));
-    if (before) W.rank[j] -= 1;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    W.first[mk] = nx;
-    W.rank[mk] = cnt;
-  }
-  __syncwarp();
-#endif
-}
+// Block-shared catalog columns.
+struct CatShared {
+  const double* lt;   // load_time_s
+  const double* p2;   // 1 / (1 + load_time / 100)
+  const double* tok;  // (double) expected_output_tokens
+  const float* p2f;   // fp32 copies for screening
+  const float* tokf;
+  const int* lex;     // rank of model_id under std::string <
+};
 
-// Replays one scenario = one reference run() (engine.cpp:76-239), REQUEST-
-// SYNCHRONOUSLY: iteration k of the loop processes request k (replay order)
-// from the moment it reaches the queue head to its service start.  This is
-// exact because, between two service starts, the reference's event loop can
-// only do the following (engine.cpp:157-230, policy.cpp:80-115):
-//   * queue empty -> the head's Arrival (a_k, 2, k) is the next relevant
-//     event; every ServiceComplete with key below it just idles its slot;
-//   * head resident & Idle -> served in the same dispatch (hit, case A);
-//   * head resident & Busy -> blocked until its own ServiceComplete; earlier
-//     completions only idle other slots (case B);
-//   * head not resident -> a free slot (case C), or an eviction decision at
-//     the current event if any slot is Idle (D1; forced when exactly one),
-//     or, if every slot is Busy, at the next ServiceComplete whose slot is
-//     then the only Idle one (forced victim, D2); then blocked until its
-//     LoadComplete (r, 0, .), before which completions only idle slots.
-// Completions are therefore applied in bulk against the event cursor, and
-// all lanes of a warp walk the same request index: the request record is a
-// warp-uniform broadcast load and divergence is confined to the case split.
-// Only D1 with >= 2 idle candidates evaluates eviction_score.
-// first/p4 are this lane's shared-memory columns (element m at [m*stride]).
-template <int C, bool DUMP>
-__device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, const Window& W,
-                                bool warp_win, double* p4tab, float* p4f, int stride,
-                                const double* s_lt, const double* s_p2, const float* s_p2f,
-                                const int* s_lex) {
+// Replays one scenario (see the file comment).  shadow lanes (warp padding)
+// replay a copy of a real scenario for lockstep and write nothing.
+template <int C, int MW, bool DUMP>
+__device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
+                                const CatShared& K) {
   const cace_scenario_t sc = P.scen[sidx];
   const int M = P.cat.M;
   const int64_t base = P.trace_off[sc.trace];
@@ -172,8 +204,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const uint32_t w = (uint32_t)sc.window_length;
   const double wd = (double)sc.window_length;
   const double unload = sc.unload_time_s;
-
+  const double norm = (double)sc.output_token_normalizer;
   const float rcpw = 1.0f / (float)sc.window_length;
+  const float w1f = (float)sc.w1;
+  const float rnormf = 1.0f / (float)sc.output_token_normalizer;
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -181,20 +215,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
   }
-  if (warp_win) window_init(W, P.first0 + (int64_t)sc.trace * M);
-  if (!is_lru) {
-    // p4 = w1 * (tokens / normalizer)   (policy.cpp:66-67); fp32 copy for screening
-    const double norm = (double)sc.output_token_normalizer;
-    for (int m = 0; m < M; ++m) {
-      const double p4 = sc.w1 * (__ldg(P.cat.tokens + m) / norm);
-      p4tab[m * stride] = p4;
-      p4f[m * stride] = (float)p4;
-    }
-  }
+  RegWindow<MW> win;
+  if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M);
 
-  // Slots (registers).  busy[s]: ServiceComplete pending at (sdone, sseq);
-  // otherwise Idle with last_used slu.  (Loading never outlives its own
-  // iteration.)
+  // Slots (registers).  Bit s of `busy`: ServiceComplete pending at
+  // (sdone, sseq); otherwise Idle with last_used slu.
   int sms[C];
   double slu[C], sdone[C];
   uint32_t sseq[C];
@@ -214,8 +239,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
   uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
-  // Software-pipelined record stream: request k+1 is fetched while k is
-  // processed (the record is a warp-uniform broadcast load).
+  // Software-pipelined record stream (warp-uniform broadcast load).
   double na = 0.0, npf = 0.0, ndc = 0.0;
   uint32_t nnxt = 0, nmc = 0;
   if (n > 0) load_rec(tr, na, npf, ndc, nnxt, nmc);
@@ -225,9 +249,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     if (k + 1 < n) load_rec(tr + k + 1, na, npf, ndc, nnxt, nmc);
     const int m = (int)(mc & 0xffffu);
 
-    // Head not yet pending (j > previous head is pending iff a_j < now):
-    // advance to its Arrival event; completions with key below it idle
-    // their slots (engine.cpp:219-230).
+    // Head not yet pending: advance to its Arrival; completions with a
+    // smaller key idle their slots (engine.cpp:219-230).
     if (!(a < cur.t)) {
 #pragma unroll
       for (int s = 0; s < C; ++s)
@@ -238,17 +261,32 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       cur = Cursor{a, 2, k};
     }
 
-    // classify (engine.cpp:163-173): resident and not Loading -> hit
+    // classify (engine.cpp:163-173): resident (never Loading here) -> hit
     int hs = -1;
 #pragma unroll
     for (int s = 0; s < C; ++s)
       if (slot_model(sms[s]) == m) hs = s;
+    const unsigned idle = ~busy & ((1u << C) - 1u);
+    const bool decide = hs < 0 && occ == C && (idle & (idle - 1u)) != 0;
+
+    // Window gather for the warp's multi-candidate decisions (collective).
+    uint32_t wfm[C], wrk[C];
+#pragma unroll
+    for (int s = 0; s < C; ++s) {
+      wfm[s] = 0xffffffffu;
+      wrk[s] = 0u;
+    }
+    if (C > 1 && warp_win && warp_any(decide && need_win)) {
+#pragma unroll
+      for (int s = 0; s < C; ++s) win.gather(slot_model(sms[s]), wfm[s], wrk[s]);
+    }
+
     double lw = 0.0;
     const bool hit = hs >= 0;
     if (hit) {
       ++hits;
       if (busy >> hs & 1u) {
-        // case B: wait for the model's own ServiceComplete
+        // blocked until the model's own ServiceComplete
         double td = 0.0;
         uint32_t tq = 0;
 #pragma unroll
@@ -268,13 +306,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     } else {
       int v;
       double ud = 0.0;
-      if (occ < C) {  // case C: free slot, no unload delay (engine.cpp:184-187)
+      if (occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
       } else {
-        const unsigned all = (1u << C) - 1u;
-        const unsigned idle = ~busy & all;
         if (idle == 0) {
-          // D2: every resident busy; the next event is the min-key
+          // every resident busy: the next event is the min-key
           // ServiceComplete, whose slot is then the only Idle one.
           int s1 = -1;
           double t1 = 0.0;
@@ -289,10 +325,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           busy &= ~(1u << s1);
           cur = Cursor{t1, 1, q1};
           v = s1;
-        } else if ((idle & (idle - 1u)) == 0) {
+        } else if (!decide) {
           v = __ffs(idle) - 1;  // exactly one candidate
         } else {
-          // ---- D1: eviction decision among >= 2 idle residents --------
+          // ---- eviction decision among >= 2 idle residents ----------
           const double now = cur.t;
           // Sorted-first = min (last_used, lex) over idle = the LRU victim.
           int f = -1;
@@ -309,29 +345,26 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           }
           v = f;
           if (!is_lru) {
-            // Window position of each slot's model: p3 = rank / w when its
-            // first pending occurrence lies in [k, min(k + w, arrived)),
-            // else 1 (policy.cpp:57-64).  Resident idle models are not the
-            // head's, so first > k.  pos[s] = rank, or -1 when outside.
+            // p3: rank / w when the model's first pending request lies in
+            // the window [k, min(k + w, arrived)), else 1 (policy.cpp:57-64).
+            // Idle residents are not the head's model, so first > k.
             int pos[C];
 #pragma unroll
             for (int s = 0; s < C; ++s) {
               pos[s] = -1;
               if (need_win) {
-                const int ms = slot_model(sms[s]);
-                const uint32_t fmv = W.first[ms];
-                bool iw = fmv < n && fmv - k < w;
-                if (iw) iw = __ldg(&tr[fmv].arrival) < now;
-                if (iw) pos[s] = (int)W.rank[ms];
+                bool iw = wfm[s] < n && wfm[s] - k < w;
+                if (iw) iw = __ldg(&tr[wfm[s]].arrival) < now;
+                if (iw) pos[s] = (int)wrk[s];
               }
             }
-            // Screening in fp32 with a rigorous bound: if one candidate's
+            // fp32 screening with a rigorous bound: if one candidate's
             // approximate total beats every other by more than the bound it
-            // is the exact arg-max.  Error of the fp32 total: |dL| <= 2.3e-5
-            // (3-ulp __logf, ln t < 70) propagates with Lipschitz constant 1
-            // through 1/(1+L); __fdividef / the rank*(1/w) product / the
-            // term conversions and three fp32 sums add <= 2^-21 (|T| + 4).
-            // The margin is twice the worst case.
+            // is the exact arg-max.  |dL| <= 2.3e-5 (3-ulp __logf, ln t < 70)
+            // propagates with Lipschitz constant 1 through 1/(1+L);
+            // __fdividef, rank*(1/w), p4 = w1*tok*(1/norm), the term
+            // conversions and three fp32 sums add <= 2^-21 (|T| + 4).  The
+            // margin is twice the worst case.
             float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
             int bs = -1;
             bool exact = false;
@@ -346,10 +379,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 const float p1v = __fdividef(1.0f, 1.0f + __logf((float)t));
                 p1 = verbatim ? p1v : 1.0f - p1v;
               }
-              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : s_p2f[ms];
+              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : K.p2f[ms];
               const float p3 =
                   variant == CACE_MINUS_P3 ? 0.0f : (pos[s] >= 0 ? (float)pos[s] * rcpw : 1.0f);
-              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : p4f[ms * stride];
+              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : w1f * K.tokf[ms] * rnormf;
               const float T = ((p1 + p2) + p3) + p4;
               if (idle >> s & 1u) {
                 tmax = fmaxf(tmax, fabsf(T));
@@ -367,9 +400,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             v = bs;
             if (exact) {
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
-              // strict max in (last_used, model_id) order" (policy.cpp:92-113),
-              // bit-identical to the reference; used on near-ties (3-11% of
-              // CACE decisions are exact ties).
+              // strict max in (last_used, model_id) order"
+              // (policy.cpp:92-113), bit-identical to the reference; taken on
+              // near-ties (3-11% of CACE decisions are exact ties).
               double tot[C];
 #pragma unroll
               for (int s = 0; s < C; ++s) {
@@ -385,10 +418,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                   const double p1v = 1.0 / (1.0 + lg);
                   p1 = verbatim ? p1v : 1.0 - p1v;
                 }
-                const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[ms];
+                const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
                 const double p3 =
                     variant == CACE_MINUS_P3 ? 0.0 : (pos[s] >= 0 ? (double)pos[s] / wd : 1.0);
-                const double p4 = variant == CACE_MINUS_P4 ? 0.0 : p4tab[ms * stride];
+                const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm);
                 tot[s] = ((p1 + p2) + p3) + p4;
               }
               v = f;
@@ -432,12 +465,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       }
       // start_load (engine.cpp:123-132), then blocked until LoadComplete
       // (r, 0, .): completions strictly before r idle their slots.
-      const double lt = s_lt[m];
+      const double lt = K.lt[m];
       const double r = (cur.t + ud) + lt;
       lw = r - cur.t;
       lo_sum += lt;
       ++loads;
-      const int word = m | (s_lex[m] << 18);
+      const int word = m | (K.lex[m] << 18);
 #pragma unroll
       for (int s = 0; s < C; ++s)
         if (s == v) sms[s] = word;
@@ -485,9 +518,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (P.dump.ttft) P.dump.ttft[o] = ttft;
       if (P.dump.e2e) P.dump.e2e[o] = e2e;
     }
-    if (warp_win) window_advance(W, m, nxt);  // head leaves the window
+    if (C > 1 && warp_win) win.advance(m, nxt);  // the head leaves the window (collective)
   }
 
+  if (shadow) return;
   cace_summary_t o;
   o.hits = hits;
   o.misses = n - hits;
@@ -504,34 +538,32 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   o.max_e2e_reasoning = me2e;
   o.eviction_hash = he;
   o.outcome_hash = ho;
-  if (shadow) return;  // warp padding lane: replayed for lockstep, no output
   P.out[sidx] = o;
   if (DUMP && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
 }
 
-#ifndef CACE_HOST_EMULATION
-// Block of LANE_BLOCK lanes (4 trace-uniform warps).  Shared memory:
-// block-shared hot catalog columns, per-lane p4 columns (fp64 exact + fp32
-// screening copy), per-warp lookahead window (first/rank).
-constexpr int LANE_BLOCK = 128;
 constexpr uint64_t kShadowBit = 1ull << 62;  // plan entry = warp padding lane
+constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 registers/lane
 
-template <int C, bool DUMP>
+#ifndef CACE_HOST_EMULATION
+constexpr int LANE_BLOCK = 128;
+
+template <int C, int MW, bool DUMP>
 __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = P.cat.M;
   double* s_lt = reinterpret_cast<double*>(smem);
   double* s_p2 = s_lt + M;
-  double* p4tab = s_p2 + M;                                          // [M][LANE_BLOCK]
-  float* s_p2f = reinterpret_cast<float*>(p4tab + (size_t)M * LANE_BLOCK);
-  float* p4f = s_p2f + M;                                            // [M][LANE_BLOCK]
-  int* s_lex = reinterpret_cast<int*>(p4f + (size_t)M * LANE_BLOCK);
-  uint32_t* wfirst = reinterpret_cast<uint32_t*>(s_lex + M);         // [4][M]
-  uint32_t* wrank = wfirst + (size_t)(LANE_BLOCK / 32) * M;          // [4][M]
+  double* s_tok = s_p2 + M;
+  float* s_p2f = reinterpret_cast<float*>(s_tok + M);
+  float* s_tokf = s_p2f + M;
+  int* s_lex = reinterpret_cast<int*>(s_tokf + M);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
+    s_tok[m] = P.cat.tokens[m];
     s_p2f[m] = (float)P.cat.p2[m];
+    s_tokf[m] = (float)P.cat.tokens[m];
     s_lex[m] = P.cat.lex[m];
   }
   __syncthreads();
@@ -542,18 +574,12 @@ __global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P)
   const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
   const int variant = P.scen[sidx].variant;
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
-  const bool warp_win = __any_sync(0xffffffffu, need_win);
-  const int warp = threadIdx.x >> 5;
-  const Window W{wfirst + (size_t)warp * M, wrank + (size_t)warp * M, M};
-  replay_scenario<C, DUMP>(P, sidx, shadow, W, warp_win, p4tab + threadIdx.x, p4f + threadIdx.x,
-                           LANE_BLOCK, s_lt, s_p2, s_p2f, s_lex);
+  const bool warp_win = __any_sync(kFull, need_win);
+  const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
+  replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K);
 }
 
-inline size_t lane_smem_bytes(int M) {
-  return (size_t)M * (8 + 8 + 4 + 4) + (size_t)M * LANE_BLOCK * (8 + 4) +
-         (size_t)(LANE_BLOCK / 32) * M * 8;
-}
-
+inline size_t lane_smem_bytes(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
 #endif  // CACE_HOST_EMULATION
 
 }  // namespace cace

@@ -39,19 +39,11 @@ using namespace cace;
 static const double kTab[256] = CACE_GLIBC_LOG_TAB;
 static const double kTab2[256] = CACE_GLIBC_LOG_TAB2;
 
-struct Scratch {
-  std::vector<uint32_t> first, rank;
-  std::vector<double> p4;
-  std::vector<float> p4f, p2f;
-};
-
 template <int C, bool D>
-static void one(const ReplayParams& P, int64_t i, Scratch& S, const double* lt, const double* p2,
-                const int* lex) {
+static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
-  const Window W{S.first.data(), S.rank.data(), P.cat.M};
-  replay_scenario<C, D>(P, i, false, W, need_win, S.p4.data(), S.p4f.data(), 1, lt, p2, S.p2f.data(), lex);
+  replay_scenario<C, 2, D>(P, i, false, need_win, K);
 }
 
 extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -89,12 +81,13 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
     P.dump.evict_model = evict_model;
     P.dump.evict_clock = evict_clock;
     P.dump.n_evict = n_evict;
-    Scratch S;
-    S.first.resize(cat.M);
-    S.rank.resize(cat.M);
-    S.p4.resize(cat.M);
-    S.p4f.resize(cat.M);
-    for (int m = 0; m < cat.M; ++m) S.p2f.push_back((float)cat.p2[m]);
+    if (cat.M > 64) return CACE_E_INVALID;
+    std::vector<float> p2f, tokf;
+    for (int m = 0; m < cat.M; ++m) {
+      p2f.push_back((float)cat.p2[m]);
+      tokf.push_back((float)cat.tok[m]);
+    }
+    const CatShared K{cat.lt.data(), cat.p2.data(), cat.tok.data(), p2f.data(), tokf.data(), lex.data()};
     for (int64_t i = 0; i < n; ++i) {
       const int32_t st = precheck(lay, sc[i]);
       const int64_t len = (sc[i].trace >= 0 && sc[i].trace < lay.T) ? lay.off[sc[i].trace + 1] - lay.off[sc[i].trace] : 0;
@@ -107,8 +100,7 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
       const int Cap = sc[i].num_accelerators * sc[i].models_per_accelerator;
       const bool D = dump_slot != nullptr;
       switch (Cap) {
-#define CASE(k) case k: D ? one<k, true>(P, i, S, cat.lt.data(), cat.p2.data(), lex.data()) \
-                          : one<k, false>(P, i, S, cat.lt.data(), cat.p2.data(), lex.data()); break;
+#define CASE(k) case k: D ? one<k, true>(P, i, K) : one<k, false>(P, i, K); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
