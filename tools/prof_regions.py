@@ -6,10 +6,10 @@ from collections import defaultdict
 
 csv_path = sys.argv[1]
 src_path = sys.argv[2] if len(sys.argv) > 2 else "paper_2506_18796_b200/csrc/replay_lane.cuh"
-MARKS = [("setup", "template <int C, bool DUMP>"), ("arrival", "Head not yet pending"),
-         ("classify", "classify (engine.cpp:163-173)"), ("caseB", "case B: wait"),
-         ("caseC/D2", "case C: free slot"), ("D1 select", "---- D1: eviction decision"),
-         ("D1 rank/window", "uint32_t fm[C];"), ("screen", "Screening in fp32"),
+MARKS = [("setup", "template <int C, bool DUMP>"), ("arrival", "Head not yet pending"), ("loop head", "Software-pipelined record stream"),
+         ("classify", "classify (engine.cpp:163-173)"), ("gather", "Window gather for the warp"), ("caseB", "blocked until the model"),
+         ("caseC/D2", "free slot, no unload delay"), ("D1 select", "---- eviction decision among"),
+         ("D1 window", "int pos[C];"), ("screen", "fp32 screening with a rigorous"),
          ("exact fp64", "Exact fp64 eviction_score"), ("evict bookkeeping", "residents.erase(victim); evictions++"),
          ("load", "start_load (engine.cpp:123-132), then"), ("serve", "start_service at now"),
          ("epilogue", "cace_summary_t o;")]
