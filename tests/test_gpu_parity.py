@@ -319,3 +319,19 @@ def test_dedup_window_and_service_times():  # test_policy.cpp:22-35, test_engine
     cat = api.ModelCatalog([api.ModelDescriptor("x", 0, 0, 1, 1, 1.0, 1024.0, 100.0, 1)])
     pf, dc = api.service_times(cat, [0, 0], [256, 256], [50, 0])
     assert pf[0] == 0.25 and dc[0] == 0.5 and dc[1] == 1.0 / 100.0
+
+
+def test_reference_side_binding_drop_in():
+    """integration/cacesim_gpu.cpp: the reference's own run()/run_grid() vs the
+    GPU-backed cacesim::gpu::run()/run_grid(), byte-identical serialisations
+    (acceptance criterion 9 standard) incl. criterion 2's 0.785513 via the GPU."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "integration", "_build", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build/adapter_test not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ADAPTER ALL_OK" in out.stdout
