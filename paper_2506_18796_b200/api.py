@@ -316,8 +316,11 @@ class SimulationReport:  # engine.hpp:46-52 (outcomes as structure-of-arrays)
     summary: np.ndarray | None = None
 
 
-def _opts(device: int = 0, log_variant: int = -1) -> N.OptsABI:
-    return N.OptsABI(device, 0, log_variant, 0, None)
+KERNEL_AUTO, KERNEL_LANE, KERNEL_WARP = 0, 1, 2
+
+
+def _opts(device: int = 0, log_variant: int = -1, kernel: int = KERNEL_AUTO) -> N.OptsABI:
+    return N.OptsABI(device, kernel, log_variant, 0, None)
 
 
 def _raise(rc: int, msg) -> None:
@@ -331,7 +334,8 @@ def _trace_array(traces):
 
 
 def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray, device: int = 0,
-              dump_scenarios=None, evict_cap: int | None = None, raise_on_error: bool = True):
+              dump_scenarios=None, evict_cap: int | None = None, raise_on_error: bool = True,
+              kernel: int = KERNEL_AUTO):
     """Replay every scenario on the GPU (host buffers in and out).
 
     Returns the summary array (SUMMARY_DTYPE); with ``dump_scenarios`` also a
@@ -354,7 +358,7 @@ def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray,
                              ptr(dump["pf"]), ptr(dump["dc"]), ptr(dump["tt"]), ptr(dump["ee"]), cap,
                              ptr(dump["em"]), ptr(dump["ec"]), ptr(dump["ne"]))
     msg = C.create_string_buffer(1024)
-    opts = _opts(device)
+    opts = _opts(device, kernel=kernel)
     rc = N.lib.cace_replay_batch(C.byref(catalog.abi()), C.cast(tarr, C.c_void_p), len(traces), ptr(scenarios),
                                  len(scenarios), ptr(summ), C.byref(dump_abi) if dump_abi else None,
                                  C.byref(opts), msg, 1024)
@@ -381,10 +385,10 @@ def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray,
 
 
 def run(trace: Trace, catalog: ModelCatalog, cluster: ClusterConfig = ClusterConfig(),
-        policy: PolicyConfig = PolicyConfig(), device: int = 0) -> SimulationReport:
+        policy: PolicyConfig = PolicyConfig(), device: int = 0, kernel: int = KERNEL_AUTO) -> SimulationReport:
     """``cacesim::run`` (engine.cpp:76-239) on the GPU: one scenario, full report."""
     sc = make_scenarios([(0, policy, cluster)])
-    _, reps = run_batch([trace], catalog, sc, device=device, dump_scenarios=[0])
+    _, reps = run_batch([trace], catalog, sc, device=device, dump_scenarios=[0], kernel=kernel)
     return reps[0]
 
 
@@ -392,13 +396,14 @@ class Engine:
     """Device-resident engine (cace_engine_*): traces uploaded once, sweeps
     replayed from device arrays.  Used by bench.py and the multi-GPU shards."""
 
-    def __init__(self, catalog: ModelCatalog, traces: list[Trace], device: int = 0, stream: int | None = None):
+    def __init__(self, catalog: ModelCatalog, traces: list[Trace], device: int = 0, stream: int | None = None,
+                 kernel: int = KERNEL_AUTO):
         self._h = C.c_void_p()
         self.catalog = catalog
         self.traces = traces
         tarr = _trace_array(traces)
         msg = C.create_string_buffer(1024)
-        opts = N.OptsABI(device, 0, -1, 0, stream)
+        opts = N.OptsABI(device, kernel, -1, 0, stream)
         rc = N.lib.cace_engine_create(C.byref(catalog.abi()), C.cast(tarr, C.c_void_p), len(traces),
                                       C.byref(opts), C.byref(self._h), msg, 1024)
         _raise(rc, msg)

@@ -16,6 +16,7 @@
 #include "glibc_log.cuh"
 #include "policy_kernels.cuh"
 #include "replay_lane.cuh"
+#include "replay_warp.cuh"
 #include "layout.hpp"
 
 using namespace cace;
@@ -153,8 +154,9 @@ struct cace_engine {
   // plan
   int64_t plan_n = -1;
   struct Seg {
-    int C;
+    int C;      // lane kernel: capacity template; warp kernel: slots per lane (1 or 2)
     int64_t b, e;
+    bool warp;  // warp-per-scenario kernel
   };
   std::vector<Seg> segs;
   DBuf<int64_t> d_order;
@@ -163,6 +165,7 @@ struct cace_engine {
   DBuf<int64_t> d_bad_idx;
   DBuf<int32_t> d_bad_code;
   int last_launches = 0;
+  int kernel_pref = CACE_KERNEL_AUTO;
   std::vector<cudaStream_t> workers;  // fork/join streams for capacity segments
   std::vector<cudaEvent_t> joins;
   cudaEvent_t fork = nullptr;
@@ -183,6 +186,7 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
     e->own_stream = true;
   }
   e->log_variant = resolve_log_variant(opts);
+  e->kernel_pref = opts ? opts->kernel : CACE_KERNEL_AUTO;
   for (int k = 0; k < kWorkers; ++k) {
     cudaStream_t ws;
     cudaEvent_t ev;
@@ -215,8 +219,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   std::vector<int64_t> ok;
   ok.reserve(n);
   for (int64_t i = 0; i < n; ++i) {
-    int32_t st = precheck(e->lay, sc[i]);
-    if (st == CACE_OK) st = precheck_pool(e->cat.M);
+    const int32_t st = precheck(e->lay, sc[i]);
     const bool tv = sc[i].trace >= 0 && sc[i].trace < e->lay.T;
     const int64_t len = tv ? e->lay.off[sc[i].trace + 1] - e->lay.off[sc[i].trace] : 0;
     if (st != CACE_OK || len == 0) {
@@ -229,36 +232,56 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   auto capof = [&](int64_t i) {
     return (int)((int64_t)sc[i].num_accelerators * sc[i].models_per_accelerator);
   };
-  // Coherent warps: capacity (template), then trace, then the control-flow
-  // shaping policy fields.
+  // Kernel choice: lane-per-scenario for capacities <= 16 and pools <= 64
+  // models (register-resident slots and window); warp-per-scenario otherwise
+  // (BASELINE config 5 regime) or when forced with CACE_KERNEL_WARP.
+  const bool force_warp = e->kernel_pref == CACE_KERNEL_WARP;
+  const bool force_lane = e->kernel_pref == CACE_KERNEL_LANE;
+  auto use_warp = [&](int64_t i) {
+    const bool lane_ok = capof(i) <= kMaxLaneC && e->cat.M <= kLaneMaxModels;
+    if (force_warp || !lane_ok) return true;
+    if (force_lane) return false;
+    return false;
+  };
+  auto key = [&](int64_t i) {  // segment key: (kernel, template parameter)
+    const int C = capof(i);
+    return use_warp(i) ? 1000 + (C <= 32 ? 1 : 2) : C;
+  };
+  // Coherent warps: segment, then trace, then the control-flow shaping
+  // policy fields.
   std::stable_sort(ok.begin(), ok.end(), [&](int64_t a, int64_t b) {
     const cace_scenario_t &x = sc[a], &y = sc[b];
-    const int ca = capof(a), cb = capof(b);
-    if (ca != cb) return ca < cb;
+    const int ka = key(a), kb = key(b);
+    if (ka != kb) return ka < kb;
     if (x.trace != y.trace) return x.trace < y.trace;
     if (x.variant != y.variant) return x.variant < y.variant;
     if (x.window_length != y.window_length) return x.window_length < y.window_length;
     return x.p1_mode < y.p1_mode;
   });
-  // Segments per capacity; inside, every (capacity, trace) group is padded
-  // to a whole number of warps with shadow lanes (copies of the group's
-  // first scenario that write nothing) so each warp is trace-uniform and can
-  // walk its trace in lockstep.
+  // Lane segments: every (capacity, trace) group is padded to a whole number
+  // of warps with shadow lanes (copies of the group's first scenario that
+  // write nothing) so each warp is trace-uniform and walks its trace in
+  // lockstep.  Warp segments need no padding (one warp = one scenario).
   std::vector<int64_t> order;
   order.reserve(ok.size() + 32 * 64);
   for (size_t k = 0; k < ok.size();) {
-    const int C = capof(ok[k]);
+    const int K = key(ok[k]);
     const int64_t seg_b = (int64_t)order.size();
     size_t j = k;
-    while (j < ok.size() && capof(ok[j]) == C) {
-      const int t = sc[ok[j]].trace;
-      size_t g = j;
-      while (g < ok.size() && capof(ok[g]) == C && sc[ok[g]].trace == t) order.push_back(ok[g++]);
-      const int64_t pad = (32 - (int64_t)(g - j) % 32) % 32;
-      for (int64_t q = 0; q < pad; ++q) order.push_back(ok[j] | (int64_t)kShadowBit);
-      j = g;
+    if (K >= 1000) {
+      while (j < ok.size() && key(ok[j]) == K) order.push_back(ok[j++]);
+      e->segs.push_back({K - 1000, seg_b, (int64_t)order.size(), true});
+    } else {
+      while (j < ok.size() && key(ok[j]) == K) {
+        const int t = sc[ok[j]].trace;
+        size_t g = j;
+        while (g < ok.size() && key(ok[g]) == K && sc[ok[g]].trace == t) order.push_back(ok[g++]);
+        const int64_t pad = (32 - (int64_t)(g - j) % 32) % 32;
+        for (int64_t q = 0; q < pad; ++q) order.push_back(ok[j] | (int64_t)kShadowBit);
+        j = g;
+      }
+      e->segs.push_back({K, seg_b, (int64_t)order.size(), false});
     }
-    e->segs.push_back({C, seg_b, (int64_t)order.size()});
     k = j;
   }
   e->d_order.upload(order.data(), order.size(), e->stream);
@@ -285,6 +308,25 @@ void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, c
 #undef CASE
     default: throw Invalid{CACE_E_INVALID, "cace: capacity not supported by the lane kernel"};
   }
+}
+
+template <int SPL, bool DUMP>
+void launch_warp(const ReplayParams& P, int64_t count, cudaStream_t s) {
+  const size_t smem = warp_smem_bytes(P.cat.M);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(replay_warp_kernel<SPL, DUMP>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per = WARP_BLOCK / 32;
+  const unsigned grid = (unsigned)((count + per - 1) / per);
+  replay_warp_kernel<SPL, DUMP><<<grid, WARP_BLOCK, smem, s>>>(P);
+  CK(cudaGetLastError());
+}
+
+void dispatch_warp(bool dump, int spl, const ReplayParams& P, int64_t count, cudaStream_t s) {
+  if (spl == 1)
+    dump ? launch_warp<1, true>(P, count, s) : launch_warp<1, false>(P, count, s);
+  else
+    dump ? launch_warp<2, true>(P, count, s) : launch_warp<2, false>(P, count, s);
 }
 
 void dispatch_lane(bool dump, int C, const ReplayParams& P, int64_t count, size_t smem,
@@ -328,7 +370,10 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
       const auto& g = e->segs[k];
       P.seg_begin = g.b;
       P.seg_end = g.e;
-      dispatch_lane(dump_on, g.C, P, g.e - g.b, smem, ws);
+      if (g.warp)
+        dispatch_warp(dump_on, g.C, P, g.e - g.b, ws);
+      else
+        dispatch_lane(dump_on, g.C, P, g.e - g.b, smem, ws);
       ++e->last_launches;
     }
     if (nseg > 1)

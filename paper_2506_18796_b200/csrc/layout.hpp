@@ -25,6 +25,7 @@ inline std::string model_name(const std::vector<std::string>& ids, int m) {
 }
 
 constexpr int kMaxLaneC = 16;  // capacities the lane kernel is instantiated for
+constexpr int kMaxWarpC = 64;  // warp kernel: <= 2 slots per lane
 
 // Host copy of the catalog columns the replay reads (catalog.hpp:13-25).
 struct HostCatalog {
@@ -157,12 +158,9 @@ inline int32_t precheck(const HostLayout& L, const cace_scenario_t& sc) {
   if (L.bad_model[sc.trace] >= 0) return CACE_E_RATES | (L.bad_model[sc.trace] << 8);
   const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
   if (cap < 1) return CACE_E_DEADLOCK;  // nothing can ever load (engine.cpp:235-237)
-  if (cap > kMaxLaneC) return CACE_E_INVALID | (2 << 8);
+  if (cap > kMaxWarpC) return CACE_E_INVALID | (2 << 8);
   return CACE_OK;
 }
-
-// Model pools beyond the lane kernel's register window (64 models).
-inline int32_t precheck_pool(int M) { return M > 64 ? (CACE_E_INVALID | (3 << 8)) : CACE_OK; }
 
 inline std::string status_text(const HostCatalog& cat, int32_t status) {
   const int code = status & 0xff;
@@ -179,8 +177,7 @@ inline std::string status_text(const HostCatalog& cat, int32_t status) {
     case CACE_E_RESIDENCY: return "run: residency bound violated";
     default:
       if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be finite and >= 0";
-      if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 16 is not supported by the lane kernel";
-      if (code == CACE_E_INVALID && m == 3) return "cace: model pools > 64 are not supported by the lane kernel";
+      if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 64 is not supported";
       return "cace: invalid scenario (bad trace index or variant)";
   }
 }
