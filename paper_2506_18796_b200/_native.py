@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libcace_gpu.so")
+LIB_PATH = os.environ.get("CACE_GPU_LIB") or os.path.join(_HERE, "lib", "libcace_gpu.so")
 
 # Status codes (include/cace_gpu.h).
 CACE_OK = 0

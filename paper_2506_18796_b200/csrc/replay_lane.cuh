@@ -219,16 +219,17 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M);
 
   // Slots (registers).  Bit s of `busy`: ServiceComplete pending at
-  // (sdone, sseq); otherwise Idle with last_used slu.
+  // (stime, sseq); otherwise Idle with last_used = stime.  One register pair
+  // serves both: a completion sets last_used to its own event time
+  // (engine.cpp:224-229), so applying it only clears the busy bit.
   int sms[C];
-  double slu[C], sdone[C];
+  double stime[C];
   uint32_t sseq[C];
   unsigned busy = 0;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
     sms[s] = 0xffff;
-    slu[s] = 0.0;
-    sdone[s] = 0.0;
+    stime[s] = 0.0;
     sseq[s] = 0;
   }
   int occ = 0;
@@ -254,9 +255,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     if (!(a < cur.t)) {
 #pragma unroll
       for (int s = 0; s < C; ++s)
-        if ((busy >> s & 1u) && sdone[s] <= a) {
+        if ((busy >> s & 1u) && stime[s] <= a) {
           busy &= ~(1u << s);
-          slu[s] = sdone[s];
         }
       cur = Cursor{a, 2, k};
     }
@@ -292,15 +292,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
         for (int s = 0; s < C; ++s)
           if (s == hs) {
-            td = sdone[s];
+            td = stime[s];
             tq = sseq[s];
           }
         cur = Cursor{td, 1, tq};
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if ((busy >> s & 1u) && sc_le(sdone[s], sseq[s], cur)) {
+          if ((busy >> s & 1u) && sc_le(stime[s], sseq[s], cur)) {
             busy &= ~(1u << s);
-            slu[s] = sdone[s];
           }
       }
     } else {
@@ -317,9 +316,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           uint32_t q1 = 0;
 #pragma unroll
           for (int s = 0; s < C; ++s)
-            if (s1 < 0 || sdone[s] < t1 || (sdone[s] == t1 && sseq[s] < q1)) {
+            if (s1 < 0 || stime[s] < t1 || (stime[s] == t1 && sseq[s] < q1)) {
               s1 = s;
-              t1 = sdone[s];
+              t1 = stime[s];
               q1 = sseq[s];
             }
           busy &= ~(1u << s1);
@@ -337,9 +336,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
           for (int s = 0; s < C; ++s) {
             const int lx = slot_lex(sms[s]);
-            if ((idle >> s & 1u) && (f < 0 || slu[s] < flu || (slu[s] == flu && lx < flex))) {
+            if ((idle >> s & 1u) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
               f = s;
-              flu = slu[s];
+              flu = stime[s];
               flex = lx;
             }
           }
@@ -373,7 +372,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               const int ms = slot_model(sms[s]);
               float p1 = 0.0f;
               if (variant != CACE_MINUS_P1) {
-                const double d = now - slu[s];
+                const double d = now - stime[s];
                 const double t = d < 1.0 ? 1.0 : d;
                 exact |= !(t < 1e30);
                 const float p1v = __fdividef(1.0f, 1.0f + __logf((float)t));
@@ -403,15 +402,20 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               // strict max in (last_used, model_id) order"
               // (policy.cpp:92-113), bit-identical to the reference; taken on
               // near-ties (3-11% of CACE decisions are exact ties).
-              double tot[C];
+              // One pass: the best non-NaN total, ties to the earlier entry in
+              // (last_used, lex) order; a NaN sorted-first entry keeps the
+              // slot (no later total compares greater than NaN).
+              bool f_nan = false;
+              double bt = 0.0, blu = 0.0;
+              int blex = 0, bv = -1;
 #pragma unroll
               for (int s = 0; s < C; ++s) {
-                tot[s] = 0.0;
                 if (!(idle >> s & 1u)) continue;
                 const int ms = slot_model(sms[s]);
+                const int lx = slot_lex(sms[s]);
                 double p1 = 0.0;
                 if (variant != CACE_MINUS_P1) {
-                  const double d = now - slu[s];
+                  const double d = now - stime[s];
                   const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
                   const double lg =
                       t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
@@ -422,28 +426,17 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 const double p3 =
                     variant == CACE_MINUS_P3 ? 0.0 : (pos[s] >= 0 ? (double)pos[s] / wd : 1.0);
                 const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm);
-                tot[s] = ((p1 + p2) + p3) + p4;
-              }
-              v = f;
-              double bt = 0.0;
-#pragma unroll
-              for (int s = 0; s < C; ++s)
-                if (s == f) bt = tot[s];
-              if (bt == bt) {  // a NaN sorted-first entry keeps the slot; NaN never wins later
-                int blex = flex;
-                double blu = flu;
-#pragma unroll
-                for (int s = 0; s < C; ++s) {
-                  const int lx = slot_lex(sms[s]);
-                  const bool earlier = slu[s] < blu || (slu[s] == blu && lx < blex);
-                  if ((idle >> s & 1u) && s != f && (tot[s] > bt || (tot[s] == bt && earlier))) {
-                    v = s;
-                    bt = tot[s];
-                    blu = slu[s];
-                    blex = lx;
-                  }
+                const double T = ((p1 + p2) + p3) + p4;
+                if (s == f) f_nan = T != T;
+                if (T == T && (bv < 0 || T > bt ||
+                               (T == bt && (stime[s] < blu || (stime[s] == blu && lx < blex))))) {
+                  bt = T;
+                  blu = stime[s];
+                  blex = lx;
+                  bv = s;
                 }
               }
+              v = f_nan ? f : bv;
             }
           }
         }
@@ -476,9 +469,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         if (s == v) sms[s] = word;
 #pragma unroll
       for (int s = 0; s < C; ++s)
-        if ((busy >> s & 1u) && sdone[s] < r) {
+        if ((busy >> s & 1u) && stime[s] < r) {
           busy &= ~(1u << s);
-          slu[s] = sdone[s];
         }
       cur = Cursor{r, 0, 0};
       hs = v;
@@ -493,7 +485,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
     for (int s = 0; s < C; ++s)
       if (s == hs) {
-        sdone[s] = done;
+        stime[s] = done;
         sseq[s] = seqc;
       }
     busy |= 1u << hs;
@@ -547,9 +539,12 @@ constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 regi
 
 #ifndef CACE_HOST_EMULATION
 constexpr int LANE_BLOCK = 128;
+#ifndef CACE_LANE_MIN_BLOCKS
+#define CACE_LANE_MIN_BLOCKS 1
+#endif
 
 template <int C, int MW, bool DUMP>
-__global__ void __launch_bounds__(LANE_BLOCK) replay_lane_kernel(ReplayParams P) {
+__global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = P.cat.M;
   double* s_lt = reinterpret_cast<double*>(smem);

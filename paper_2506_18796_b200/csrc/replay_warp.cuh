@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   // Slots owned by this lane: global slot id g = lane + 32 j.
   int smodel[SPL], slex[SPL];
   bool sbusy[SPL], svalid[SPL];
-  double slu[SPL], sdone[SPL];
+  double stime[SPL];  // busy: ServiceComplete time; idle: last_used (same value once applied)
   uint32_t sseq[SPL];
 #pragma unroll
   for (int j = 0; j < SPL; ++j) {
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
     slex[j] = 0;
     sbusy[j] = false;
     svalid[j] = lane + 32 * j < C;
-    slu[j] = sdone[j] = 0.0;
+    stime[j] = 0.0;
     sseq[j] = 0;
   }
   int occ = 0;
@@ -124,9 +124,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
     if (!(a < cur.t)) {  // head's Arrival into an empty queue
 #pragma unroll
       for (int j = 0; j < SPL; ++j)
-        if (sbusy[j] && sdone[j] <= a) {
+        if (sbusy[j] && stime[j] <= a) {
           sbusy[j] = false;
-          slu[j] = sdone[j];
         }
       cur = Cursor{a, 2, k};
     }
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
 #pragma unroll
       for (int j = 0; j < SPL; ++j) {
         const bool b = __shfl_sync(kFull, sbusy[j], ol);
-        const double d = __shfl_sync(kFull, sdone[j], ol);
+        const double d = __shfl_sync(kFull, stime[j], ol);
         const uint32_t q = __shfl_sync(kFull, sseq[j], ol);
         if (j == oj) {
           hb = b;
@@ -160,9 +159,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
         cur = Cursor{td, 1, tq};
 #pragma unroll
         for (int j = 0; j < SPL; ++j)
-          if (sbusy[j] && sc_le(sdone[j], sseq[j], cur)) {
+          if (sbusy[j] && sc_le(stime[j], sseq[j], cur)) {
             sbusy[j] = false;
-            slu[j] = sdone[j];
           }
       }
     } else {
@@ -185,8 +183,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
           int bg = -1;
 #pragma unroll
           for (int j = 0; j < SPL; ++j)
-            if (svalid[j] && key_lt(sdone[j], sseq[j], bd, bq)) {
-              bd = sdone[j];
+            if (svalid[j] && key_lt(stime[j], sseq[j], bd, bq)) {
+              bd = stime[j];
               bq = sseq[j];
               bg = lane + 32 * j;
             }
@@ -224,8 +222,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             tnan[j] = false;
             if (!(svalid[j] && !sbusy[j])) continue;
             const int g = lane + 32 * j;
-            if (slu[j] < flu || (slu[j] == flu && slex[j] < flex)) {
-              flu = slu[j];
+            if (stime[j] < flu || (stime[j] == flu && slex[j] < flex)) {
+              flu = stime[j];
               flex = slex[j];
               fg = g;
             }
@@ -233,7 +231,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             const int ms = smodel[j];
             double p1 = 0.0;
             if (variant != CACE_MINUS_P1) {
-              const double d = now - slu[j];
+              const double d = now - stime[j];
               const double t = d < 1.0 ? 1.0 : d;
               const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
               const double p1v = 1.0 / (1.0 + lg);
@@ -250,9 +248,9 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (s_tok[ms] / norm);
             const double T = ((p1 + p2) + p3) + p4;
             if (T == T && (bg < 0 || T > bt ||
-                           (T == bt && (slu[j] < blu || (slu[j] == blu && slex[j] < blex))))) {
+                           (T == bt && (stime[j] < blu || (stime[j] == blu && slex[j] < blex))))) {
               bt = T;
-              blu = slu[j];
+              blu = stime[j];
               blex = slex[j];
               bg = g;
             }
@@ -326,9 +324,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
           slex[j] = s_lex[m];
           sbusy[j] = false;
         }
-        if (sbusy[j] && sdone[j] < r) {
+        if (sbusy[j] && stime[j] < r) {
           sbusy[j] = false;
-          slu[j] = sdone[j];
         }
       }
       cur = Cursor{r, 0, 0};
@@ -345,7 +342,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
     for (int j = 0; j < SPL; ++j)
       if (lane + 32 * j == hs) {
         sbusy[j] = true;
-        sdone[j] = done;
+        stime[j] = done;
         sseq[j] = seqc;
       }
     ++seqc;
