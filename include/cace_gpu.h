@@ -120,11 +120,13 @@ typedef struct {
   uint64_t n_completion, n_reasoning;
   double sum_ttft_completion, sum_e2e_reasoning;
   double max_ttft_completion, max_e2e_reasoning;
-  uint64_t eviction_hash; /* fold over evictions: mix(mix(h, victim_model), bits(clock)) */
-  uint64_t outcome_hash;  /* fold over requests in replay order: mix(mix(h, bits(ttft)), bits(e2e) ^ cold) */
+  uint64_t eviction_hash; /* fold over evictions: h = mix(h, bits(clock) ^ (victim_model << 32)) */
+  uint64_t outcome_hash;  /* fold over requests in replay order:
+                             h = mix(h, bits(ttft) ^ swap32(bits(e2e)) ^ cold) */
 } cace_summary_t;
 
-/* CACE_HASH: h0 = 0x6a09e667f3bcc909; mix(h,x) = (h ^= x, h *= 0xbf58476d1ce4e5b9, h ^ (h >> 31)). */
+/* CACE_HASH: h0 = 0x6a09e667f3bcc909; mix(h,x) = (h ^= x, h *= 0xbf58476d1ce4e5b9, h ^ (h >> 31));
+ * swap32(u) = u rotated by 32 bits. */
 #define CACE_HASH_SEED 0x6a09e667f3bcc909ULL
 #define CACE_HASH_MUL 0xbf58476d1ce4e5b9ULL
 

@@ -251,7 +251,7 @@ int32_t port_run(const port_catalog_t* cat, const double* arrival, const int32_t
         resident--;
         if (evict_model && S->evictions < (uint64_t)evict_cap) evict_model[S->evictions] = victim;
         if (evict_clock && S->evictions < (uint64_t)evict_cap) evict_clock[S->evictions] = now;
-        S->eviction_hash = mix(mix(S->eviction_hash, (uint64_t)victim), bits(now));
+        S->eviction_hash = mix(S->eviction_hash, bits(now) ^ ((uint64_t)victim << 32));
         S->evictions++;
         unload = sc->unload_time_s;
       }
@@ -284,7 +284,8 @@ int32_t port_run(const port_catalog_t* cat, const double* arrival, const int32_t
         S->sum_e2e_reasoning += ee[r];
         if (ee[r] > S->max_e2e_reasoning) S->max_e2e_reasoning = ee[r];
       }
-      S->outcome_hash = mix(mix(S->outcome_hash, bits(tt[r])), bits(ee[r]) ^ (uint64_t)cold[r]);
+      const uint64_t e = bits(ee[r]);
+      S->outcome_hash = mix(S->outcome_hash, bits(tt[r]) ^ ((e << 32) | (e >> 32)) ^ (uint64_t)cold[r]);
     }
     for (int64_t i = 0; i < n; ++i) {
       if (cold_out) cold_out[i] = cold[i];

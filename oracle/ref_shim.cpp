@@ -230,14 +230,13 @@ void summarize_report(const SimulationReport& rep, const Trace& t, const ModelCa
       s->sum_e2e_reasoning += o.e2e_s;
       if (o.e2e_s > s->max_e2e_reasoning) s->max_e2e_reasoning = o.e2e_s;
     }
-    h = mix(h, bits(o.ttft_s));
-    h = mix(h, bits(o.e2e_s) ^ (o.cold_start ? 1ULL : 0ULL));
+    const uint64_t e = bits(o.e2e_s);
+    h = mix(h, bits(o.ttft_s) ^ ((e << 32) | (e >> 32)) ^ (o.cold_start ? 1ULL : 0ULL));
   }
   s->outcome_hash = h;
   uint64_t he = kHashSeed;
   for (size_t k = 0; k < victims.size(); ++k) {
-    he = mix(he, static_cast<uint64_t>(model_index(cat, victims[k])));
-    he = mix(he, bits(clocks[k]));
+    he = mix(he, bits(clocks[k]) ^ (static_cast<uint64_t>(model_index(cat, victims[k])) << 32));
   }
   s->eviction_hash = he;
 }

@@ -149,7 +149,7 @@ struct cace_engine {
   HostLayout lay;  // host replay-order layout (rec/perm/first0 freed after upload)
   DBuf<ReqRec> d_rec;
   DBuf<int64_t> d_off;
-  DBuf<uint32_t> d_first0, d_perm;
+  DBuf<uint32_t> d_first0, d_perm, d_ncomp;
   DBuf<double> d_tab, d_tab2;
   // plan
   int64_t plan_n = -1;
@@ -204,6 +204,7 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
   e->d_off.upload(e->lay.off.data(), e->lay.off.size(), s);
   e->d_first0.upload(e->lay.first0.data(), e->lay.first0.size(), s);
   e->d_perm.upload(e->lay.perm.data(), e->lay.perm.size(), s);
+  e->d_ncomp.upload(e->lay.ncomp.data(), e->lay.ncomp.size(), s);
   e->d_tab.upload(kLogTab, 256, s);
   e->d_tab2.upload(kLogTab2, 256, s);
   CK(cudaStreamSynchronize(s));
@@ -293,6 +294,9 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
 
 template <int C, int MW, bool DUMP>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DUMP>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
   replay_lane_kernel<C, MW, DUMP><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
@@ -347,6 +351,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   P.trace_off = e->d_off.p;
   P.first0 = e->d_first0.p;
   P.perm = e->d_perm.p;
+  P.trace_ncomp = e->d_ncomp.p;
   P.cat = e->cat.dev();
   P.log_tab = e->d_tab.p;
   P.log_tab2 = e->d_tab2.p;
@@ -355,7 +360,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   P.order = e->d_order.p;
   P.out = d_out;
   P.dump = dump;
-  const size_t smem = lane_smem_bytes(e->cat.M);
+  const int M = e->cat.M;
   e->last_launches = 0;
   // Capacity segments are independent kernels: fork them over the engine's
   // worker streams so they share the SMs (one segment alone is often less
@@ -373,7 +378,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
       if (g.warp)
         dispatch_warp(dump_on, g.C, P, g.e - g.b, ws);
       else
-        dispatch_lane(dump_on, g.C, P, g.e - g.b, smem, ws);
+        dispatch_lane(dump_on, g.C, P, g.e - g.b, lane_smem_bytes(M, g.C), ws);
       ++e->last_launches;
     }
     if (nseg > 1)

@@ -77,6 +77,7 @@ struct HostLayout {
   std::vector<uint32_t> perm;      // [N] sorted position -> caller's request index
   std::vector<uint32_t> first0;    // [T][M] first sorted index of each model (n if absent)
   std::vector<int32_t> bad_model;  // [T] model of the first request with bad rates, or -1
+  std::vector<uint32_t> ncomp;     // [T] completion-class requests
 };
 
 inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int32_t n_traces,
@@ -95,6 +96,7 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
   L.perm.assign(N, 0);
   L.first0.assign((size_t)n_traces * M, 0);
   L.bad_model.assign(n_traces, -1);
+  L.ncomp.assign(n_traces, 0);
   std::vector<uint32_t> last(M);
   for (int t = 0; t < n_traces; ++t) {
     const cace_trace_t& tr = traces[t];
@@ -135,6 +137,7 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
       r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
       last[m] = (uint32_t)k;
       L.perm[b + k] = i;
+      L.ncomp[t] += cat.cls[m] == CACE_REASONING ? 0u : 1u;
       if (cat.bad_rates(m)) L.bad_model[t] = m;  // ends as the first in replay order
     }
     for (int m = 0; m < M; ++m) L.first0[(size_t)t * M + m] = last[m];

@@ -57,6 +57,7 @@ __device__ __forceinline__ uint64_t hmix(uint64_t h, uint64_t x) {
   return h ^ (h >> 31);
 }
 __device__ __forceinline__ uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
+__device__ __forceinline__ uint64_t swap32(uint64_t u) { return (u << 32) | (u >> 32); }
 
 __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf, double& dc,
                                          uint32_t& nxt, uint32_t& mc) {
@@ -187,11 +188,19 @@ struct CatShared {
   const int* lex;     // rank of model_id under std::string <
 };
 
+// Per-lane shared-memory columns (element i at [i * stride]).
+struct LaneSmem {
+  float* p4f;        // [M] p4 = w1 * (tokens / normalizer), fp32 (screening)
+  uint32_t* seq;     // [C] ServiceComplete push seq of each busy slot
+  uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
+  int stride;
+};
+
 // Replays one scenario (see the file comment).  shadow lanes (warp padding)
 // replay a copy of a real scenario for lockstep and write nothing.
 template <int C, int MW, bool DUMP>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
-                                const CatShared& K) {
+                                const CatShared& K, const LaneSmem& S) {
   const cace_scenario_t sc = P.scen[sidx];
   const int M = P.cat.M;
   const int64_t base = P.trace_off[sc.trace];
@@ -206,8 +215,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const double unload = sc.unload_time_s;
   const double norm = (double)sc.output_token_normalizer;
   const float rcpw = 1.0f / (float)sc.window_length;
-  const float w1f = (float)sc.w1;
-  const float rnormf = 1.0f / (float)sc.output_token_normalizer;
+  const int st = S.stride;
+  for (int mm = 0; mm < M; ++mm) {
+    S.slot_of[mm * st] = 0;
+    // fp32 copy of the exact p4 (policy.cpp:66-67), for screening only
+    if (!is_lru) S.p4f[mm * st] = (float)(sc.w1 * (K.tok[mm] / norm));
+  }
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -219,24 +232,24 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M);
 
   // Slots (registers).  Bit s of `busy`: ServiceComplete pending at
-  // (stime, sseq); otherwise Idle with last_used = stime.  One register pair
-  // serves both: a completion sets last_used to its own event time
-  // (engine.cpp:224-229), so applying it only clears the busy bit.
+  // (stime, seq[s]); otherwise Idle with last_used = stime.  One register
+  // pair serves both: a completion sets last_used to its own event time
+  // (engine.cpp:224-229), so applying it only clears the busy bit.  The push
+  // seq (tie-break of equal completion times) lives in shared memory.
   int sms[C];
   double stime[C];
-  uint32_t sseq[C];
   unsigned busy = 0;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
     sms[s] = 0xffff;
     stime[s] = 0.0;
-    sseq[s] = 0;
   }
   int occ = 0;
   uint32_t seqc = 0;
   Cursor cur{-INFINITY, 2, 0};
 
-  uint32_t hits = 0, evictions = 0, loads = 0, nc = 0, nr = 0;
+  // loads == misses == n - hits; evictions == loads - final occupancy.
+  uint32_t hits = 0;
   double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
   uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
@@ -262,10 +275,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     }
 
     // classify (engine.cpp:163-173): resident (never Loading here) -> hit
-    int hs = -1;
-#pragma unroll
-    for (int s = 0; s < C; ++s)
-      if (slot_model(sms[s]) == m) hs = s;
+    int hs = (int)S.slot_of[m * st] - 1;
     const unsigned idle = ~busy & ((1u << C) - 1u);
     const bool decide = hs < 0 && occ == C && (idle & (idle - 1u)) != 0;
 
@@ -288,19 +298,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (busy >> hs & 1u) {
         // blocked until the model's own ServiceComplete
         double td = 0.0;
-        uint32_t tq = 0;
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if (s == hs) {
-            td = stime[s];
-            tq = sseq[s];
-          }
+          if (s == hs) td = stime[s];
+        const uint32_t tq = S.seq[hs * st];
         cur = Cursor{td, 1, tq};
 #pragma unroll
         for (int s = 0; s < C; ++s)
-          if ((busy >> s & 1u) && sc_le(stime[s], sseq[s], cur)) {
+          if ((busy >> s & 1u) && (stime[s] < td || (stime[s] == td && S.seq[s * st] <= tq)))
             busy &= ~(1u << s);
-          }
       }
     } else {
       int v;
@@ -311,16 +317,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         if (idle == 0) {
           // every resident busy: the next event is the min-key
           // ServiceComplete, whose slot is then the only Idle one.
-          int s1 = -1;
-          double t1 = 0.0;
-          uint32_t q1 = 0;
+          int s1 = 0;
+          double t1 = stime[0];
 #pragma unroll
-          for (int s = 0; s < C; ++s)
-            if (s1 < 0 || stime[s] < t1 || (stime[s] == t1 && sseq[s] < q1)) {
+          for (int s = 1; s < C; ++s)
+            if (stime[s] < t1 || (stime[s] == t1 && S.seq[s * st] < S.seq[s1 * st])) {
               s1 = s;
               t1 = stime[s];
-              q1 = sseq[s];
             }
+          const uint32_t q1 = S.seq[s1 * st];
           busy &= ~(1u << s1);
           cur = Cursor{t1, 1, q1};
           v = s1;
@@ -329,21 +334,26 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         } else {
           // ---- eviction decision among >= 2 idle residents ----------
           const double now = cur.t;
-          // Sorted-first = min (last_used, lex) over idle = the LRU victim.
-          int f = -1;
-          double flu = 0.0;
-          int flex = 0;
+          // Sorted-first = min (last_used, lex) over idle: the LRU victim,
+          // and the NaN rule of the exact CACE path.
+          auto sorted_first = [&]() {
+            int f = -1;
+            double flu = 0.0;
+            int flex = 0;
 #pragma unroll
-          for (int s = 0; s < C; ++s) {
-            const int lx = slot_lex(sms[s]);
-            if ((idle >> s & 1u) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
-              f = s;
-              flu = stime[s];
-              flex = lx;
+            for (int s = 0; s < C; ++s) {
+              const int lx = slot_lex(sms[s]);
+              if ((idle >> s & 1u) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
+                f = s;
+                flu = stime[s];
+                flex = lx;
+              }
             }
-          }
-          v = f;
-          if (!is_lru) {
+            return f;
+          };
+          if (is_lru) {
+            v = sorted_first();
+          } else {
             // p3: rank / w when the model's first pending request lies in
             // the window [k, min(k + w, arrived)), else 1 (policy.cpp:57-64).
             // Idle residents are not the head's model, so first > k.
@@ -381,7 +391,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               const float p2 = variant == CACE_MINUS_P2 ? 0.0f : K.p2f[ms];
               const float p3 =
                   variant == CACE_MINUS_P3 ? 0.0f : (pos[s] >= 0 ? (float)pos[s] * rcpw : 1.0f);
-              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : w1f * K.tokf[ms] * rnormf;
+              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : S.p4f[ms * st];
               const float T = ((p1 + p2) + p3) + p4;
               if (idle >> s & 1u) {
                 tmax = fmaxf(tmax, fabsf(T));
@@ -405,6 +415,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               // One pass: the best non-NaN total, ties to the earlier entry in
               // (last_used, lex) order; a NaN sorted-first entry keeps the
               // slot (no later total compares greater than NaN).
+              const int f = sorted_first();
               bool f_nan = false;
               double bt = 0.0, blu = 0.0;
               int blex = 0, bv = -1;
@@ -445,8 +456,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
         for (int s = 0; s < C; ++s)
           if (s == v) vm = slot_model(sms[s]);
-        ++evictions;
-        he = hmix(hmix(he, (uint64_t)vm), dbits(cur.t));
+        S.slot_of[vm * st] = 0;
+        he = hmix(he, dbits(cur.t) ^ ((uint64_t)vm << 32));
         if (DUMP && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
@@ -462,11 +473,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       const double r = (cur.t + ud) + lt;
       lw = r - cur.t;
       lo_sum += lt;
-      ++loads;
       const int word = m | (K.lex[m] << 18);
 #pragma unroll
       for (int s = 0; s < C; ++s)
         if (s == v) sms[s] = word;
+      S.slot_of[m * st] = (uint8_t)(v + 1);
 #pragma unroll
       for (int s = 0; s < C; ++s)
         if ((busy >> s & 1u) && stime[s] < r) {
@@ -484,22 +495,18 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const double done = (now + pf) + dc;
 #pragma unroll
     for (int s = 0; s < C; ++s)
-      if (s == hs) {
-        stime[s] = done;
-        sseq[s] = seqc;
-      }
+      if (s == hs) stime[s] = done;
+    S.seq[hs * st] = seqc;
     busy |= 1u << hs;
     ++seqc;
     if ((mc >> 16) == CACE_COMPLETION) {
-      ++nc;
       sttft += ttft;
       mttft = ttft > mttft ? ttft : mttft;
     } else {
-      ++nr;
       se2e += e2e;
       me2e = e2e > me2e ? e2e : me2e;
     }
-    ho = hmix(hmix(ho, dbits(ttft)), dbits(e2e) ^ (hit ? 0ull : 1ull));
+    ho = hmix(ho, dbits(ttft) ^ swap32(dbits(e2e)) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0) {
       const int64_t o = doff + P.perm[base + k];
       if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
@@ -517,13 +524,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   cace_summary_t o;
   o.hits = hits;
   o.misses = n - hits;
-  o.evictions = evictions;
-  o.loads = loads;
+  o.evictions = n - hits - (uint32_t)occ;  // every load after the fill evicts
+  o.loads = n - hits;                      // loads == misses (test_engine.cpp:168)
   o.load_overhead_s = lo_sum;
   o.max_resident = occ;
   o.status = CACE_OK;
-  o.n_completion = nc;
-  o.n_reasoning = nr;
+  o.n_completion = P.trace_ncomp[sc.trace];
+  o.n_reasoning = n - P.trace_ncomp[sc.trace];
   o.sum_ttft_completion = sttft;
   o.sum_e2e_reasoning = se2e;
   o.max_ttft_completion = mttft;
@@ -553,6 +560,9 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   float* s_p2f = reinterpret_cast<float*>(s_tok + M);
   float* s_tokf = s_p2f + M;
   int* s_lex = reinterpret_cast<int*>(s_tokf + M);
+  float* l_p4f = reinterpret_cast<float*>(s_lex + M);                   // [M][LANE_BLOCK]
+  uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_p4f + (size_t)M * LANE_BLOCK);  // [C][LANE_BLOCK]
+  uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_seq + (size_t)C * LANE_BLOCK);   // [M][LANE_BLOCK]
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
@@ -571,10 +581,13 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
   const bool warp_win = __any_sync(kFull, need_win);
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
-  replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K);
+  const LaneSmem S{l_p4f + threadIdx.x, l_seq + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK};
+  replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);
 }
 
-inline size_t lane_smem_bytes(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
+inline size_t lane_smem_bytes(int M, int C) {
+  return (size_t)M * (3 * 8 + 2 * 4 + 4) + (size_t)LANE_BLOCK * (M * 4 + C * 4 + M);
+}
 #endif  // CACE_HOST_EMULATION
 
 }  // namespace cace

@@ -43,6 +43,7 @@ struct ReplayParams {
   const int64_t* trace_off; // [T+1]
   const uint32_t* first0;   // [T][M] first sorted index of each model
   const uint32_t* perm;     // sorted index -> caller's request index
+  const uint32_t* trace_ncomp;  // [T] completion-class requests per trace
   DevCatalog cat;
   const double* log_tab;
   const double* log_tab2;

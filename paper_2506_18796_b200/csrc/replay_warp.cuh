@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
           if ((v >> 5) == j) vm = mm;
         }
         ++evictions;
-        he = hmix(hmix(he, (uint64_t)vm), dbits(cur.t));
+        he = hmix(he, dbits(cur.t) ^ ((uint64_t)vm << 32));
         if (DUMP && dslot >= 0 && lane == 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
       se2e += e2e;
       me2e = e2e > me2e ? e2e : me2e;
     }
-    ho = hmix(hmix(ho, dbits(ttft)), dbits(e2e) ^ (hit ? 0ull : 1ull));
+    ho = hmix(ho, dbits(ttft) ^ swap32(dbits(e2e)) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0 && lane == 0) {
       const int64_t o = doff + P.perm[base + k];
       if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;

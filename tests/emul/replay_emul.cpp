@@ -43,7 +43,11 @@ template <int C, bool D>
 static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
-  replay_scenario<C, 2, D>(P, i, false, need_win, K);
+  std::vector<float> p4f(P.cat.M);
+  std::vector<uint32_t> seq(C);
+  std::vector<uint8_t> slot_of(P.cat.M);
+  const LaneSmem S{p4f.data(), seq.data(), slot_of.data(), 1};
+  replay_scenario<C, 2, D>(P, i, false, need_win, K, S);
 }
 
 extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -64,6 +68,7 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
     P.trace_off = lay.off.data();
     P.first0 = lay.first0.data();
     P.perm = lay.perm.data();
+    P.trace_ncomp = lay.ncomp.data();
     P.cat = DevCatalog{cat.M, cat.lt.data(), cat.p2.data(), cat.tok.data(), lex.data()};
     P.log_tab = kTab;
     P.log_tab2 = kTab2;
