@@ -218,8 +218,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const int st = S.stride;
   for (int mm = 0; mm < M; ++mm) {
     S.slot_of[mm * st] = 0;
-    // fp32 copy of the exact p4 (policy.cpp:66-67), for screening only
-    if (!is_lru) S.p4f[mm * st] = (float)(sc.w1 * (K.tok[mm] / norm));
+    // fp32 p2 + p4 of model mm (policy.cpp:55, 66-67), for screening only;
+    // ablated terms are 0 exactly as the reference zeroes them
+    if (!is_lru) {
+      const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[mm];
+      const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[mm] / norm);
+      S.p4f[mm * st] = (float)(p2 + p4);
+    }
   }
 
   int dslot = -1;
@@ -279,16 +284,23 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const unsigned idle = ~busy & ((1u << C) - 1u);
     const bool decide = hs < 0 && occ == C && (idle & (idle - 1u)) != 0;
 
-    // Window gather for the warp's multi-candidate decisions (collective).
-    uint32_t wfm[C], wrk[C];
+    // Window position of every slot's model for the warp's multi-candidate
+    // decisions (collective gather): p3 = rank / w when the model's first
+    // pending request lies in the window [k, min(k + w, arrived)), else 1
+    // (policy.cpp:57-64).  Idle residents are not the head's model, so
+    // first > k.  pos[s] = rank, or -1 outside the window.
+    int pos[C];
 #pragma unroll
-    for (int s = 0; s < C; ++s) {
-      wfm[s] = 0xffffffffu;
-      wrk[s] = 0u;
-    }
+    for (int s = 0; s < C; ++s) pos[s] = -1;
     if (C > 1 && warp_win && warp_any(decide && need_win)) {
 #pragma unroll
-      for (int s = 0; s < C; ++s) win.gather(slot_model(sms[s]), wfm[s], wrk[s]);
+      for (int s = 0; s < C; ++s) {
+        uint32_t fmv, rk;
+        win.gather(slot_model(sms[s]), fmv, rk);
+        bool iw = need_win && fmv < n && fmv - k < w;
+        if (iw) iw = __ldg(&tr[fmv].arrival) < cur.t;
+        if (iw) pos[s] = (int)rk;
+      }
     }
 
     double lw = 0.0;
@@ -303,10 +315,21 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           if (s == hs) td = stime[s];
         const uint32_t tq = S.seq[hs * st];
         cur = Cursor{td, 1, tq};
+        // completions with key <= (td, 1, tq); equal times (rare) break ties
+        // on the push seq.
+        unsigned done_m = 1u << hs, eq = 0u;
 #pragma unroll
-        for (int s = 0; s < C; ++s)
-          if ((busy >> s & 1u) && (stime[s] < td || (stime[s] == td && S.seq[s * st] <= tq)))
-            busy &= ~(1u << s);
+        for (int s = 0; s < C; ++s) {
+          done_m |= (stime[s] < td) ? (1u << s) : 0u;
+          eq |= (stime[s] == td && s != hs) ? (1u << s) : 0u;
+        }
+        eq &= busy;
+        while (eq) {
+          const int s = __ffs(eq) - 1;
+          eq &= eq - 1u;
+          if (S.seq[s * st] <= tq) done_m |= 1u << s;
+        }
+        busy &= ~done_m;
       }
     } else {
       int v;
@@ -354,19 +377,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           if (is_lru) {
             v = sorted_first();
           } else {
-            // p3: rank / w when the model's first pending request lies in
-            // the window [k, min(k + w, arrived)), else 1 (policy.cpp:57-64).
-            // Idle residents are not the head's model, so first > k.
-            int pos[C];
-#pragma unroll
-            for (int s = 0; s < C; ++s) {
-              pos[s] = -1;
-              if (need_win) {
-                bool iw = wfm[s] < n && wfm[s] - k < w;
-                if (iw) iw = __ldg(&tr[wfm[s]].arrival) < now;
-                if (iw) pos[s] = (int)wrk[s];
-              }
-            }
             // fp32 screening with a rigorous bound: if one candidate's
             // approximate total beats every other by more than the bound it
             // is the exact arg-max.  |dL| <= 2.3e-5 (3-ulp __logf, ln t < 70)
@@ -382,17 +392,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               const int ms = slot_model(sms[s]);
               float p1 = 0.0f;
               if (variant != CACE_MINUS_P1) {
-                const double d = now - stime[s];
-                const double t = d < 1.0 ? 1.0 : d;
-                exact |= !(t < 1e30);
-                const float p1v = __fdividef(1.0f, 1.0f + __logf((float)t));
+                const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
+                exact |= !(t < 1e30f);
+                const float p1v = __fdividef(1.0f, 1.0f + __logf(t));
                 p1 = verbatim ? p1v : 1.0f - p1v;
               }
-              const float p2 = variant == CACE_MINUS_P2 ? 0.0f : K.p2f[ms];
               const float p3 =
                   variant == CACE_MINUS_P3 ? 0.0f : (pos[s] >= 0 ? (float)pos[s] * rcpw : 1.0f);
-              const float p4 = variant == CACE_MINUS_P4 ? 0.0f : S.p4f[ms * st];
-              const float T = ((p1 + p2) + p3) + p4;
+              const float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
               if (idle >> s & 1u) {
                 tmax = fmaxf(tmax, fabsf(T));
                 exact |= !(fabsf(T) <= 1e6f);  // NaN / inf / huge: decide exactly
