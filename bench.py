@@ -37,8 +37,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--requests", type=int, default=100_000)
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
+                    help="BASELINE config: 4 = 1M scenarios x 100k (default), 5 = 256-model pool, 10M bursty")
+    ap.add_argument("--requests", type=int, default=None, help="requests per trace (cfg4 100k, cfg5 10M)")
     ap.add_argument("--seeds", type=int, default=32)
+    ap.add_argument("--scenarios", type=int, default=8192, help="cfg5 scenario count")
     ap.add_argument("--vectors-stride", type=int, default=1, help="subsample the 4096 weight vectors (debug)")
     ap.add_argument("--cpu-sample", type=int, default=48, help="scenarios in the CPU-baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -54,6 +57,8 @@ def dist_env():
 def workload(args):
     from paper_2506_18796_b200 import synth
 
+    if args.config == 5:
+        return synth.config5(n_requests=args.requests, n_scenarios=args.scenarios)
     catalog = synth.eight_model_catalog()
     traces = [synth.mixed_trace(catalog, args.requests, seed=1 + s) for s in range(args.seeds)]
     pols = synth.weight_vectors_cfg3()[:: args.vectors_stride]
@@ -171,6 +176,8 @@ def run_reference_arm(args):
 
 def main():
     args = parse()
+    if args.requests is None:
+        args.requests = 10_000_000 if args.config == 5 else 100_000
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -308,8 +315,10 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests"
-                               % (args.seeds, n_req),
+        "config": {"workload": ("BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests"
+                                % (args.seeds, n_req)) if args.config == 4 else
+                               ("BASELINE config 5: %d scenarios x %d-request bursty trace, 256 CodeLLMs, capacity 32, "
+                                "window 1024" % (S_total, n_req)),
                    "scenarios": S_total, "requests_per_trace": n_req, "models": len(catalog),
                    "parallelism": f"scenario shards x{world}", "l2": "flushed (256 MB write) before every step",
                    "vectors_stride": args.vectors_stride},

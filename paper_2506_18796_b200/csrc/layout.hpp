@@ -113,6 +113,8 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
         throw Invalid{CACE_E_INVALID, "cace: non-finite arrival_time_s"};
       if (tr.prompt_tokens[i] < 0)  // a negative prefill would run the event clock backwards
         throw Invalid{CACE_E_INVALID, "cace: negative prompt_tokens"};
+      if (!(std::fabs(tr.arrival_time_s[i]) < 1e20))  // keeps every event time < 1e30
+        throw Invalid{CACE_E_INVALID, "cace: |arrival_time_s| must be < 1e20"};
     }
     // Replay order = Arrival pop order (time, seq = index) (engine.cpp:49-55).
     std::vector<uint32_t> ord(n);
@@ -142,6 +144,13 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
     }
     for (int m = 0; m < M; ++m) L.first0[(size_t)t * M + m] = last[m];
   }
+  // Event times stay < 1e30 (the kernels' fp32 screening relies on it): the
+  // clock advances by at most one load (+ unload) and one service per request.
+  double worst = 0.0;
+  for (int m = 0; m < M; ++m) worst = std::max(worst, cat.lt[m]);
+  for (const ReqRec& r : L.rec) worst = std::max(worst, r.prefill + r.decode);
+  if (!(worst * (double)(N + 1) < 1e28))
+    throw Invalid{CACE_E_INVALID, "cace: load/service times too large (event clock would exceed 1e28 s)"};
 }
 
 // Reference run() preconditions (engine.cpp:79-92, 17-20) for one scenario:
@@ -154,7 +163,7 @@ inline int32_t precheck(const HostLayout& L, const cace_scenario_t& sc) {
   if (sc.num_accelerators < 1) return CACE_E_ACCELERATORS;
   // A negative unload delay can schedule a LoadComplete before the current
   // event (time running backwards); the engine requires a monotone clock.
-  if (!(sc.unload_time_s >= 0.0) || !std::isfinite(sc.unload_time_s))
+  if (!(sc.unload_time_s >= 0.0 && sc.unload_time_s < 1e15))
     return CACE_E_INVALID | (1 << 8);
   const int64_t n = L.off[sc.trace + 1] - L.off[sc.trace];
   if (n == 0) return CACE_OK;
@@ -179,7 +188,7 @@ inline std::string status_text(const HostCatalog& cat, int32_t status) {
       return "run: deadlock \xe2\x80\x94 pending requests with no schedulable event";
     case CACE_E_RESIDENCY: return "run: residency bound violated";
     default:
-      if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be finite and >= 0";
+      if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be in [0, 1e15)";
       if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 64 is not supported";
       return "cace: invalid scenario (bad trace index or variant)";
   }

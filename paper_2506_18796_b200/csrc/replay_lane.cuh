@@ -216,6 +216,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const double norm = (double)sc.output_token_normalizer;
   const float rcpw = 1.0f / (float)sc.window_length;
   const int st = S.stride;
+  // fp32 screening is valid while every p2 + p4 is finite and moderate; the
+  // event clock is finite (validated on the host) and t < 1e30 below.
+  bool screen_ok = true;
   for (int mm = 0; mm < M; ++mm) {
     S.slot_of[mm * st] = 0;
     // fp32 p2 + p4 of model mm (policy.cpp:55, 66-67), for screening only;
@@ -224,6 +227,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[mm];
       const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[mm] / norm);
       S.p4f[mm * st] = (float)(p2 + p4);
+      screen_ok = screen_ok && fabs(p2 + p4) <= 1e5;  // false for NaN / inf
     }
   }
 
@@ -386,14 +390,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             // margin is twice the worst case.
             float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
             int bs = -1;
-            bool exact = false;
+            bool exact = !screen_ok;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
               const int ms = slot_model(sms[s]);
               float p1 = 0.0f;
               if (variant != CACE_MINUS_P1) {
                 const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
-                exact |= !(t < 1e30f);
                 const float p1v = __fdividef(1.0f, 1.0f + __logf(t));
                 p1 = verbatim ? p1v : 1.0f - p1v;
               }
@@ -402,7 +405,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               const float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
               if (idle >> s & 1u) {
                 tmax = fmaxf(tmax, fabsf(T));
-                exact |= !(fabsf(T) <= 1e6f);  // NaN / inf / huge: decide exactly
                 if (T > best) {
                   second = best;
                   best = T;
@@ -554,7 +556,7 @@ constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 regi
 #ifndef CACE_HOST_EMULATION
 constexpr int LANE_BLOCK = 128;
 #ifndef CACE_LANE_MIN_BLOCKS
-#define CACE_LANE_MIN_BLOCKS 1
+#define CACE_LANE_MIN_BLOCKS 4  // <= 128 registers: 4 blocks (16 warps) per SM; measured +4% vs uncapped
 #endif
 
 template <int C, int MW, bool DUMP>

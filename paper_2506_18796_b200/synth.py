@@ -108,3 +108,23 @@ def config2(n_requests: int = 10_000, seed: int = 1, capacity: int = 3):
     rows = [(0, PolicyConfig(variant=v, output_token_normalizer=catalog.max_expected_output_tokens()),
              ClusterConfig(num_accelerators=capacity)) for v in (Variant.CACE_FULL, Variant.LRU)]
     return catalog, traces, make_scenarios(rows)
+
+
+def config5(n_requests: int = 10_000_000, n_scenarios: int = 8192, capacity: int = 32, window: int = 1024):
+    """BASELINE config 5: 256 CodeLLMs, one bursty (MMPP) trace, long window,
+    capacity 32; scenarios = w1 x {cace, -p1, -p2, -p4} x P1 mode x unload
+    delay (n_scenarios of that grid).  Needs the warp-per-scenario kernel."""
+    catalog = ModelCatalog.synthetic_pool(256, seed=5)
+    traces = [mixed_trace(catalog, n_requests, seed=1, rate=40.0, bursty=True)]
+    rows = []
+    variants = (Variant.CACE_FULL, Variant.CACE_MINUS_P1, Variant.CACE_MINUS_P2, Variant.CACE_MINUS_P4)
+    per = max(1, n_scenarios // (len(variants) * 2 * 16))
+    for variant in variants:
+        for p1 in (P1Mode.PROSE_CONSISTENT, P1Mode.VERBATIM):
+            for u in range(16):
+                for w1 in np.linspace(0.0, 2.0, per):
+                    rows.append((0, PolicyConfig(variant=variant, w1=float(w1), window_length=window,
+                                                 output_token_normalizer=catalog.max_expected_output_tokens(),
+                                                 p1_mode=p1),
+                                 ClusterConfig(num_accelerators=capacity, unload_time_s=0.25 * u)))
+    return catalog, traces, make_scenarios(rows[:n_scenarios])
