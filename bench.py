@@ -106,28 +106,41 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(catalog, traces, sc, sample: int, seed: int = 12345):
-    """The reference run() (oracle/_ref) on all host threads over a bounded
-    random sample of the same sweep; also the parity sample."""
-    from oracle import ref
-    from tests.helpers import ref_catalog, ref_scenario, ref_trace
-
-    rng = np.random.default_rng(seed)
-    idx = np.sort(rng.choice(len(sc), size=min(sample, len(sc)), replace=False))
-    rcat = ref_catalog(ref, catalog)
+def _cpu_replay(catalog, traces, sc, idx, threads):
+    """Replay scenarios sc[idx] on the host CPU: the reference run()
+    (oracle/_ref) when the catalog is reference-expressible (<= 16 models keyed
+    by language x task), else the C restatement (oracle/cace_port.c, checked
+    bit-exact against the reference).  Returns (summaries, seconds, kind)."""
     used = sorted({int(sc[i]["trace"]) for i in idx})
     remap = {t: k for k, t in enumerate(used)}
-    rows = []
-    for i in idx:
-        r = ref_scenario(ref, sc[i])
-        r.trace = remap[int(sc[i]["trace"])]
-        rows.append(r)
-    threads = ref.max_threads()
-    summ, secs = ref.run_batch(rcat, [ref_trace(traces[t]) for t in used], rows, threads=threads)
+    rows = sc[idx].copy()
+    rows["trace"] = [remap[int(t)] for t in rows["trace"]]
+    if len(catalog) <= 16:
+        from oracle import ref
+        from tests.helpers import ref_catalog, ref_scenario, ref_trace
+
+        summ, secs = ref.run_batch(ref_catalog(ref, catalog), [ref_trace(traces[t]) for t in used],
+                                   [ref_scenario(ref, r) for r in rows], threads=threads)
+        return summ, secs, "reference"
+    from oracle import port
+
+    summ, secs = port.run_batch(port.Catalog(catalog), [traces[t] for t in used], rows, threads=threads)
+    return summ, secs, "port"
+
+
+def cpu_baseline(catalog, traces, sc, sample: int, seed: int = 12345):
+    """The CPU simulator on all host threads over a bounded random sample of
+    the same sweep; also the parity sample."""
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(len(sc), size=min(sample, len(sc)), replace=False))
+    threads = os.cpu_count() or 1
+    summ, secs, kind = _cpu_replay(catalog, traces, sc, idx, threads)
     n_req = sum(len(traces[int(sc[i]["trace"])]) for i in idx)
-    return idx, summ, {"value": n_req / secs, "unit": "scenario-requests/s", "cores": threads, "kind": "reference",
+    return idx, summ, {"value": n_req / secs, "unit": "scenario-requests/s", "cores": threads, "kind": kind,
                        "sample": f"{len(idx)} random scenarios of the same sweep x {len(traces[0])} requests "
-                                 f"({n_req:.3g} scenario-requests, {secs:.2f} s, reference run() on std::thread fan-out)"}
+                                 f"({n_req:.3g} scenario-requests, {secs:.2f} s, "
+                                 f"{'reference run()' if kind == 'reference' else 'C restatement'} "
+                                 f"on a std::thread/pthread fan-out)"}
 
 
 def run_reference_arm(args):
@@ -140,23 +153,14 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcace_ref.so not built"}))
         return
     catalog, traces, sc = workload(args)
-    from tests.helpers import ref_catalog, ref_scenario, ref_trace
-
-    rcat = ref_catalog(ref, catalog)
-    threads = ref.max_threads()
-    per_step = max(2 * threads, 8)
+    threads = os.cpu_count() or 1
+    per_step = max(2 * threads, 8) if args.config == 4 else max(threads // 4, 2)
     rng = np.random.default_rng(777)
     times, reqs = [], []
+    kind = "reference"
     for step in range(args.warmup + args.steps):
-        idx = rng.choice(len(sc), size=per_step, replace=False)
-        used = sorted({int(sc[i]["trace"]) for i in idx})
-        remap = {t: k for k, t in enumerate(used)}
-        rows = []
-        for i in idx:
-            r = ref_scenario(ref, sc[i])
-            r.trace = remap[int(sc[i]["trace"])]
-            rows.append(r)
-        _, secs = ref.run_batch(rcat, [ref_trace(traces[t]) for t in used], rows, threads=threads)
+        idx = np.sort(rng.choice(len(sc), size=per_step, replace=False))
+        _, secs, kind = _cpu_replay(catalog, traces, sc, idx, threads)
         if step >= args.warmup:
             times.append(secs)
             reqs.append(per_step * args.requests)
@@ -166,9 +170,9 @@ def run_reference_arm(args):
         "unit": "scenario-requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "BASELINE config 4 (1M scenarios x 100k requests), bounded random sample per step",
-                   "requests": args.requests, "seeds": args.seeds, "scenarios_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": "scenario-requests/s", "cores": threads, "kind": "reference",
+        "config": {"workload": f"BASELINE config {args.config}, bounded random sample per step",
+                   "requests": args.requests, "scenarios_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "scenario-requests/s", "cores": threads, "kind": kind,
                          "sample": f"{per_step} random scenarios x {args.requests} requests per step"},
         "e2e": {"value": value, "unit": "scenario-requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -302,7 +306,7 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         try:
             idx, rsumm, cpu = cpu_baseline(catalog, traces, sc_all, args.cpu_sample)
-            from tests.helpers import SUMMARY_FLOAT_KEYS, SUMMARY_KEYS
+            from tests.helpers import SUMMARY_FLOAT_KEYS, SUMMARY_KEYS  # noqa: F811
 
             gs = summ[idx]
             ok = all((gs[k] == rsumm[k]).all() for k in SUMMARY_KEYS) and all(
