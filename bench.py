@@ -188,11 +188,34 @@ def main():
     import torch
 
     rank, world, local = dist_env()
+    # NCCL over NVLink on a real multi-GPU box; CACE_DIST_BACKEND=gloo lets
+    # the multi-rank flow run with several ranks sharing one GPU (tests).
+    backend = os.environ.get("CACE_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def coll(x):  # tensor on the collective's device
+        return x if backend == "nccl" else x.cpu()
+
+    def all_reduce(x, op):
+        y = coll(x)
+        torch.distributed.all_reduce(y, op=op)
+        return y
+
+    def all_gather_bytes(buf):
+        if backend == "nccl":
+            torch.distributed.all_gather_into_tensor(gathered, buf)
+            return gathered
+        parts = [torch.empty(buf.numel(), dtype=torch.uint8) for _ in range(world)]
+        torch.distributed.all_gather(parts, buf.cpu())
+        return torch.cat(parts)
     import paper_2506_18796_b200 as P
     from paper_2506_18796_b200 import SUMMARY_DTYPE
 
@@ -227,7 +250,7 @@ def main():
         launches = eng.replay_device(d_sc.data_ptr(), len(sc), d_out.data_ptr(), stream.cuda_stream)
         if world > 1:
             pad[: d_out.numel()].copy_(d_out)
-            torch.distributed.all_gather_into_tensor(gathered, pad)
+            all_gather_bytes(pad)
         return launches
 
     for _ in range(args.warmup):
@@ -251,7 +274,7 @@ def main():
     t_local = float(np.mean(ms))
     t = torch.tensor([t_local], device="cuda")
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = all_reduce(t, torch.distributed.ReduceOp.MAX)
     t_max = float(t.item())
     value = S_total * n_req / (t_max / 1e3)
     summ = d_out.cpu().numpy().view(SUMMARY_DTYPE)
@@ -259,7 +282,7 @@ def main():
     evictions = int(summ["evictions"].sum())
     if world > 1:
         ev = torch.tensor([evictions], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(ev)
+        ev = all_reduce(ev, torch.distributed.ReduceOp.SUM)
         evictions = int(ev.item())
 
     # ---- end to end through the public API (host buffers, H2D/D2H inside) ----
@@ -269,18 +292,17 @@ def main():
         for k in range(args.e2e_steps + 1):
             barrier()
             t0 = time.perf_counter()
-            host_summ = P.run_batch(traces, catalog, sc)
+            host_summ = P.run_batch(traces, catalog, sc, device=local)
             if world > 1:
                 hs = torch.from_numpy(host_summ.view(np.uint8)).cuda()
                 pad[: hs.numel()].copy_(hs)
-                torch.distributed.all_gather_into_tensor(gathered, pad)
-                gathered.cpu()
+                all_gather_bytes(pad).cpu()
             barrier()
             if k > 0:  # first call warms the CUDA context / allocator
                 e2e_ms.append(1e3 * (time.perf_counter() - t0))
         tl = torch.tensor([float(np.mean(e2e_ms))], device="cuda")
         if world > 1:
-            torch.distributed.all_reduce(tl, op=torch.distributed.ReduceOp.MAX)
+            tl = all_reduce(tl, torch.distributed.ReduceOp.MAX)
         n_all = sum(len(t) for t in traces)
         h2d = n_all * (8 + 4 + 4 + 4) + len(sc) * sc.dtype.itemsize
         d2h = len(sc) * SUMMARY_DTYPE.itemsize
