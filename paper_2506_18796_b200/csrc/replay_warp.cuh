@@ -30,6 +30,20 @@ namespace cace {
 
 constexpr int WARP_BLOCK = 128;  // 4 scenarios per block
 
+// Order-preserving unsigned key of a non-NaN double (-0.0 folded onto +0.0,
+// which compare equal in the reference's doubles).
+__device__ __forceinline__ uint64_t okey(double d) {
+  const uint64_t u = (uint64_t)__double_as_longlong(d + 0.0);
+  return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+
+// Warp-wide max of a 64-bit key with two 32-bit redux.sync reductions.
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t k) {
+  const uint32_t hi = __reduce_max_sync(kFull, (uint32_t)(k >> 32));
+  const uint32_t lo = __reduce_max_sync(kFull, (uint32_t)(k >> 32) == hi ? (uint32_t)k : 0u);
+  return ((uint64_t)hi << 32) | lo;
+}
+
 // (d, q) < (d2, q2) lexicographically
 __device__ __forceinline__ bool key_lt(double d, uint32_t q, double d2, uint32_t q2) {
   return d < d2 || (d == d2 && q < q2);
@@ -209,23 +223,21 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
         } else {
           // ---- eviction decision: each lane scores its idle slots ----
           const double now = cur.t;
-          // sorted-first f = min (last_used, lex) over idle (warp reduction)
-          double flu = INFINITY;
-          int flex = 0x7fffffff, fg = -1;
-          // best = first strict max (see policy.cpp:102-113), candidates
-          // compared by (total desc, last_used asc, lex asc), NaN never wins
-          double bt = -INFINITY, blu = 0.0;
-          int blex = 0, bg = -1;
+          // Per lane: the best own candidate by (total desc, last_used asc,
+          // lex asc) over non-NaN totals, its own sorted-first by
+          // (last_used, lex), and whether any own total is NaN.
+          double bt = 0.0, blu = 0.0, flu = 0.0;
+          int blex = 0, bj = -1, flex = 0, fj = -1;
+          bool has_nan = false;
           bool tnan[SPL];
 #pragma unroll
           for (int j = 0; j < SPL; ++j) {
             tnan[j] = false;
             if (!(svalid[j] && !sbusy[j])) continue;
-            const int g = lane + 32 * j;
-            if (stime[j] < flu || (stime[j] == flu && slex[j] < flex)) {
+            if (fj < 0 || stime[j] < flu || (stime[j] == flu && slex[j] < flex)) {
               flu = stime[j];
               flex = slex[j];
-              fg = g;
+              fj = j;
             }
             if (is_lru) continue;
             const int ms = smodel[j];
@@ -247,50 +259,53 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             }
             const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (s_tok[ms] / norm);
             const double T = ((p1 + p2) + p3) + p4;
-            if (T == T && (bg < 0 || T > bt ||
+            tnan[j] = T != T;
+            has_nan |= tnan[j];
+            if (T == T && (bj < 0 || T > bt ||
                            (T == bt && (stime[j] < blu || (stime[j] == blu && slex[j] < blex))))) {
               bt = T;
               blu = stime[j];
               blex = slex[j];
-              bg = g;
-            }
-            tnan[j] = T != T;
-          }
-          // reduce sorted-first
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            const double o_lu = __shfl_xor_sync(kFull, flu, off);
-            const int o_lex = __shfl_xor_sync(kFull, flex, off);
-            const int o_g = __shfl_xor_sync(kFull, fg, off);
-            if (o_g >= 0 && (fg < 0 || o_lu < flu || (o_lu == flu && o_lex < flex))) {
-              flu = o_lu;
-              flex = o_lex;
-              fg = o_g;
+              bj = j;
             }
           }
-          v = fg;
-          if (!is_lru) {
-            // is the sorted-first entry's total NaN? (its owner knows)
-            bool fn = false;
-#pragma unroll
-            for (int j = 0; j < SPL; ++j)
-              if (lane + 32 * j == fg) fn = tnan[j];
-            const bool first_nan = __any_sync(kFull, fn);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const double o_t = __shfl_xor_sync(kFull, bt, off);
-              const double o_lu = __shfl_xor_sync(kFull, blu, off);
-              const int o_lex = __shfl_xor_sync(kFull, blex, off);
-              const int o_g = __shfl_xor_sync(kFull, bg, off);
-              if (o_g >= 0 && (bg < 0 || o_t > bt ||
-                               (o_t == bt && (o_lu < blu || (o_lu == blu && o_lex < blex))))) {
-                bt = o_t;
-                blu = o_lu;
-                blex = o_lex;
-                bg = o_g;
-              }
+          // Sorted-first across the warp: min (last_used, lex) via redux.
+          auto sorted_first = [&]() {
+            const uint64_t kl = fj >= 0 ? ~okey(flu) : 0ull;  // max of ~key = min of key
+            const uint64_t mx = warp_max_u64(kl);
+            const bool tie = fj >= 0 && kl == mx;
+            const uint32_t lx = __reduce_min_sync(kFull, tie ? (uint32_t)flex : 0xffffffffu);
+            const unsigned who = __ballot_sync(kFull, tie && (uint32_t)flex == lx);
+            const int ol = __ffs(who) - 1;
+            return ol + 32 * __shfl_sync(kFull, fj, ol);
+          };
+          if (is_lru) {
+            v = sorted_first();
+          } else {
+            // first strict max in sorted order (policy.cpp:102-113) = max
+            // non-NaN total, ties to the smaller (last_used, lex) ...
+            const uint64_t kt = bj >= 0 ? okey(bt) : 0ull;
+            const uint64_t mt = warp_max_u64(kt);
+            unsigned tied = __ballot_sync(kFull, bj >= 0 && kt == mt);
+            if (tied & (tied - 1u)) {  // exact tie across lanes (rare)
+              const bool in = (tied >> lane) & 1u;
+              const uint64_t kl = in ? ~okey(blu) : 0ull;
+              const uint64_t mx = warp_max_u64(kl);
+              const bool t2 = in && kl == mx;
+              const uint32_t lx = __reduce_min_sync(kFull, t2 ? (uint32_t)blex : 0xffffffffu);
+              tied = __ballot_sync(kFull, t2 && (uint32_t)blex == lx);
             }
-            if (!first_nan && bg >= 0) v = bg;
+            const int ol = __ffs(tied) - 1;
+            v = ol + 32 * __shfl_sync(kFull, bj, ol);
+            // ... unless the sorted-first entry's total is NaN: it keeps the slot.
+            if (__any_sync(kFull, has_nan)) {
+              const int f = sorted_first();
+              bool fn = false;
+#pragma unroll
+              for (int j = 0; j < SPL; ++j)
+                if (lane + 32 * j == f) fn = tnan[j];
+              if (__any_sync(kFull, fn)) v = f;
+            }
           }
         }
         // evict v (engine.cpp:205-206)
