@@ -58,3 +58,16 @@ def test_config5_shape_vs_port(cap):
     got = P.run_batch(traces, catalog, sc)
     want, _ = port.run_batch(port.Catalog(catalog), traces, sc)
     assert_summaries_equal(got, want, f"config-5 shape C={cap}")
+
+
+def test_lane_and_warp_kernels_agree_at_scale():
+    """Both kernels on 4096 config-4-grid scenarios x 20k requests: identical summaries."""
+    import paper_2506_18796_b200 as P
+    from paper_2506_18796_b200 import api, synth
+
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 20_000, seed=s) for s in (21, 22)]
+    sc = synth.scenario_grid(synth.weight_vectors_cfg3()[::16], range(1, 9), 2, 600)
+    a = P.run_batch(traces, catalog, sc, kernel=api.KERNEL_LANE)
+    b = P.run_batch(traces, catalog, sc, kernel=api.KERNEL_WARP)
+    assert_summaries_equal(a, b, "lane vs warp at scale")
