@@ -122,13 +122,17 @@ typedef struct {
   double max_ttft_completion, max_e2e_reasoning;
   uint64_t eviction_hash; /* fold over evictions: h = mix(h, bits(clock) ^ (victim_model << 32)) */
   uint64_t outcome_hash;  /* fold over requests in replay order:
-                             h = mix(h, bits(ttft) ^ swap32(bits(e2e)) ^ cold) */
+                             h = mix(h, bits(ttft) ^ cold) */
 } cace_summary_t;
 
-/* CACE_HASH: h0 = 0x6a09e667f3bcc909; mix(h,x) = (h ^= x, h *= 0xbf58476d1ce4e5b9, h ^ (h >> 31));
- * swap32(u) = u rotated by 32 bits. */
+/* CACE_HASH: h0 = 0x6a09e667f3bcc909; mix(h, x) updates the two 32-bit halves
+ * independently as polynomial hashes (mod 2^32):
+ *   lo(h') = lo(h) * 0x9e3779b1 + lo(x),  hi(h') = hi(h) * 0x85ebca77 + hi(x).
+ * Both multipliers are odd, so mix is a bijection in h for a fixed x and any
+ * single differing term changes the final value. */
 #define CACE_HASH_SEED 0x6a09e667f3bcc909ULL
-#define CACE_HASH_MUL 0xbf58476d1ce4e5b9ULL
+#define CACE_HASH_MUL_LO 0x9e3779b1u
+#define CACE_HASH_MUL_HI 0x85ebca77u
 
 /* Optional full dump for a few scenarios: per-request RequestOutcome fields
  * (engine.hpp:19-30) indexed by the caller's request index, and the

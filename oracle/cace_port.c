@@ -76,9 +76,10 @@ static Event heap_pop(Heap* h) {
 }
 
 static inline uint64_t mix(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= 0xbf58476d1ce4e5b9ULL;
-  return h ^ (h >> 31);
+  /* CACE_HASH, include/cace_gpu.h */
+  const uint32_t lo = (uint32_t)h * 0x9e3779b1u + (uint32_t)x;
+  const uint32_t hi = (uint32_t)(h >> 32) * 0x85ebca77u + (uint32_t)(x >> 32);
+  return ((uint64_t)hi << 32) | lo;
 }
 static inline uint64_t bits(double d) {
   uint64_t u;
@@ -284,8 +285,7 @@ int32_t port_run(const port_catalog_t* cat, const double* arrival, const int32_t
         S->sum_e2e_reasoning += ee[r];
         if (ee[r] > S->max_e2e_reasoning) S->max_e2e_reasoning = ee[r];
       }
-      const uint64_t e = bits(ee[r]);
-      S->outcome_hash = mix(S->outcome_hash, bits(tt[r]) ^ ((e << 32) | (e >> 32)) ^ (uint64_t)cold[r]);
+      S->outcome_hash = mix(S->outcome_hash, bits(tt[r]) ^ (uint64_t)cold[r]);
     }
     for (int64_t i = 0; i < n; ++i) {
       if (cold_out) cold_out[i] = cold[i];

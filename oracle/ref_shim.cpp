@@ -145,10 +145,10 @@ void put_msg(char* msg, size_t cap, const std::string& s) {
 
 // Summary hash: the spec documented at include/cace_gpu.h (CACE_HASH_*).
 inline uint64_t mix(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= 0xbf58476d1ce4e5b9ULL;
-  h ^= h >> 31;
-  return h;
+  /* CACE_HASH, include/cace_gpu.h */
+  const uint32_t lo = (uint32_t)h * 0x9e3779b1u + (uint32_t)x;
+  const uint32_t hi = (uint32_t)(h >> 32) * 0x85ebca77u + (uint32_t)(x >> 32);
+  return ((uint64_t)hi << 32) | lo;
 }
 inline uint64_t bits(double d) {
   uint64_t u;
@@ -230,8 +230,7 @@ void summarize_report(const SimulationReport& rep, const Trace& t, const ModelCa
       s->sum_e2e_reasoning += o.e2e_s;
       if (o.e2e_s > s->max_e2e_reasoning) s->max_e2e_reasoning = o.e2e_s;
     }
-    const uint64_t e = bits(o.e2e_s);
-    h = mix(h, bits(o.ttft_s) ^ ((e << 32) | (e >> 32)) ^ (o.cold_start ? 1ULL : 0ULL));
+    h = mix(h, bits(o.ttft_s) ^ (o.cold_start ? 1ULL : 0ULL));
   }
   s->outcome_hash = h;
   uint64_t he = kHashSeed;

@@ -111,6 +111,10 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
                       "catalog: no model registered for model index " + std::to_string(m)};
       if (!std::isfinite(tr.arrival_time_s[i]))
         throw Invalid{CACE_E_INVALID, "cace: non-finite arrival_time_s"};
+      // parse_trace rejects negative arrivals (workload.cpp:245-248); the
+      // kernels' sign-encoded slot times rely on a non-negative clock.
+      if (tr.arrival_time_s[i] < 0)
+        throw Invalid{CACE_E_INVALID, "cace: negative arrival_time_s"};
       if (tr.prompt_tokens[i] < 0)  // a negative prefill would run the event clock backwards
         throw Invalid{CACE_E_INVALID, "cace: negative prompt_tokens"};
       if (!(std::fabs(tr.arrival_time_s[i]) < 1e20))  // keeps every event time < 1e30
@@ -136,6 +140,7 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
       r.prefill = (double)tr.prompt_tokens[i] / cat.pr[m];
       r.decode = (double)std::max(tr.output_tokens[i], 1) / cat.dr[m];
       r.nxt = last[m];
+      r.nxa = last[m] < (uint32_t)n ? L.rec[b + last[m]].arrival : INFINITY;
       r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
       last[m] = (uint32_t)k;
       L.perm[b + k] = i;

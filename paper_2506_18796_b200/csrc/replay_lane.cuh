@@ -5,7 +5,7 @@
 // host plan makes every warp trace-uniform (capacity/trace groups padded to
 // whole warps with shadow lanes), and the replay loop is organised so that
 // iteration k of EVERY lane processes request k of the trace — the request
-// record is a warp-uniform broadcast load and the lanes never drift apart.
+// record is a warp-uniform broadcast read and the lanes never drift apart.
 //
 // Why request k can be processed in one step (the reference's min-heap order
 // (time, kind, seq) of engine.cpp:49-55; kind 0 LoadComplete, 1
@@ -30,12 +30,24 @@
 // queue is the contiguous range [k, arrived), and only a decision with >= 2
 // idle candidates evaluates eviction_score.
 //
+// Slot state is one register per slot, SIGN-ENCODED: stime >= 0 is an Idle
+// slot with last_used_s = stime; stime < 0 is a Busy slot whose
+// ServiceComplete is at -stime (a completion sets last_used to its own event
+// time, engine.cpp:224-229, so applying it is |stime|).  Event times are
+// >= 0 (arrivals are validated non-negative, as parse_trace requires,
+// workload.cpp:245) and service completions are > 0, so the sign is free.
+//
 // Lookahead window (dedup_window, policy.cpp:22-37): p3 of a resident model
-// m needs first[m] (first replay index >= k requesting m) and rank(m) =
-// #{m' : first[m'] < first[m]}.  Both depend only on the trace and k, so they
-// are warp-wide state held in registers distributed over the lanes (lane j
-// owns models j, j+32, ...); they are gathered with shuffles when some lane
-// of the warp faces a decision and advanced with one ballot/popc per request.
+// m needs first[m] (first replay index >= k requesting m), rank(m) =
+// #{m' : first[m'] < first[m]} and whether first[m] has arrived.  These
+// depend only on the trace and k, so they are warp-wide: lane j owns models
+// j, j+32 in registers, advances them with one ballot/popc per request and
+// publishes {first, rank, arrival of first} to a per-warp shared-memory table
+// that deciding lanes read with one 128-bit load per candidate.
+//
+// The trace is staged per warp in shared memory by cp.async (32-record
+// chunks, double-buffered), so the per-request record read is a broadcast
+// shared load and no registers carry a prefetched record.
 //
 // All fp64 arithmetic uses the reference's operation order with no
 // contraction (built with -fmad=false); P1's log is the glibc restatement
@@ -51,13 +63,13 @@
 
 namespace cace {
 
+// Summary fingerprint (spec CACE_HASH in include/cace_gpu.h).
 __device__ __forceinline__ uint64_t hmix(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= CACE_HASH_MUL;
-  return h ^ (h >> 31);
+  const uint32_t lo = (uint32_t)h * CACE_HASH_MUL_LO + (uint32_t)x;
+  const uint32_t hi = (uint32_t)(h >> 32) * CACE_HASH_MUL_HI + (uint32_t)(x >> 32);
+  return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
-__device__ __forceinline__ uint64_t swap32(uint64_t u) { return (u << 32) | (u >> 32); }
 
 __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf, double& dc,
                                          uint32_t& nxt, uint32_t& mc) {
@@ -74,6 +86,7 @@ __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf,
 // Slot word: model (bits 0-15) | lex rank of model_id (bits 18-31).
 __device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
 __device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
+__device__ __forceinline__ bool is_idle(double st) { return __double2hiint(st) >= 0; }
 
 // Event key (time, kind, seq) of engine.cpp:49-55.
 struct Cursor {
@@ -88,28 +101,56 @@ __device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
 }
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr float kLn2f = 0.693147180559945309f;
+
+#ifdef CACE_HOST_EMULATION
+__device__ __forceinline__ float fast_lg2(float x) { return log2f(x); }
+__device__ __forceinline__ float fast_rcp(float x) { return 1.0f / x; }
+#else
+__device__ __forceinline__ float fast_lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+#endif
+
+// Per-warp window table entry: first pending index of the model, its rank
+// among the models' first occurrences (as a float: an exact small integer),
+// and that request's arrival time (+inf when the model has no pending
+// request left).
+struct alignas(16) WinEnt {
+  uint32_t f;
+  float r;
+  double fa;
+};
 
 // Warp-wide lookahead window (see the file comment).  MW registers per lane:
 // lane j owns models j + 32q, q < MW.
 template <int MW>
-struct RegWindow {
+struct Window {
 #ifdef CACE_HOST_EMULATION
   uint32_t f[32 * MW], r[32 * MW];
+  double fa[32 * MW];
   int M;
-  void init(const uint32_t* f0, int M_) {
+  void init(const uint32_t* f0, int M_, const ReqRec* tr, uint32_t n, WinEnt*) {
     M = M_;
-    for (int m = 0; m < M; ++m) f[m] = f0[m];
+    for (int m = 0; m < M; ++m) {
+      f[m] = f0[m];
+      fa[m] = f0[m] < n ? tr[f0[m]].arrival : INFINITY;
+    }
     for (int m = 0; m < M; ++m) {
       uint32_t c = 0;
       for (int q = 0; q < M; ++q) c += f0[q] < f0[m] ? 1u : 0u;
       r[m] = c;
     }
   }
-  void gather(int ms, uint32_t& fm, uint32_t& rk) const {
-    fm = ms < M ? f[ms] : 0xffffffffu;
-    rk = ms < M ? r[ms] : 0u;
-  }
-  void advance(int mk, uint32_t nx) {
+  WinEnt gather(int ms) const { return WinEnt{f[ms], (float)r[ms], fa[ms]}; }
+  void advance(int mk, uint32_t nx, double nxa) {
     uint32_t cnt = 0;
     for (int j = 0; j < M; ++j)
       if (j != mk && f[j] < nx) {
@@ -118,12 +159,16 @@ struct RegWindow {
       }
     f[mk] = nx;
     r[mk] = cnt;
+    fa[mk] = nxa;
   }
 #else
   uint32_t f[MW], r[MW];
   int M;
-  __device__ __forceinline__ void init(const uint32_t* f0, int M_) {
+  WinEnt* tab;
+  __device__ __forceinline__ void init(const uint32_t* f0, int M_, const ReqRec* tr, uint32_t n,
+                                       WinEnt* tab_) {
     M = M_;
+    tab = tab_;
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < MW; ++q) {
@@ -132,25 +177,14 @@ struct RegWindow {
       uint32_t c = 0;
       for (int mm = 0; mm < M; ++mm) c += __ldg(f0 + mm) < f[q] ? 1u : 0u;
       r[q] = c;
+      if (m < M) tab[m] = WinEnt{f[q], (float)c, f[q] < n ? __ldg(&tr[f[q]].arrival) : INFINITY};
     }
+    __syncwarp();
   }
-  // Collective (all 32 lanes): this lane reads model ms's (first, rank).
-  __device__ __forceinline__ void gather(int ms, uint32_t& fm, uint32_t& rk) const {
-    const int src = ms & 31, qq = ms >> 5;
-    fm = 0xffffffffu;
-    rk = 0u;
-#pragma unroll
-    for (int q = 0; q < MW; ++q) {
-      const uint32_t a = __shfl_sync(kFull, f[q], src);
-      const uint32_t b = __shfl_sync(kFull, r[q], src);
-      if (q == qq) {
-        fm = a;
-        rk = b;
-      }
-    }
-  }
-  // Collective: the head (model mk) is served; mk's first becomes nx.
-  __device__ __forceinline__ void advance(int mk, uint32_t nx) {
+  // Per lane (no collective): model ms's entry.
+  __device__ __forceinline__ WinEnt gather(int ms) const { return tab[ms]; }
+  // Collective: the head (model mk) is served; mk's first becomes nx (arrival nxa).
+  __device__ __forceinline__ void advance(int mk, uint32_t nx, double nxa) {
     const int lane = threadIdx.x & 31;
     uint32_t cnt = 0;
 #pragma unroll
@@ -161,22 +195,61 @@ struct RegWindow {
       if (before) r[q] -= 1;
     }
 #pragma unroll
-    for (int q = 0; q < MW; ++q)
-      if (lane + 32 * q == mk) {
+    for (int q = 0; q < MW; ++q) {
+      const int m = lane + 32 * q;
+      if (m == mk) {
         f[q] = nx;
         r[q] = cnt;
+        tab[m].fa = nxa;
       }
+      if (m < M) *reinterpret_cast<uint2*>(&tab[m]) = make_uint2(f[q], __float_as_uint((float)r[q]));
+    }
+    __syncwarp();
   }
 #endif
 };
 
-__device__ __forceinline__ bool warp_any(bool p) {
+// Trace records of the warp's trace in replay order.  Device: per-warp
+// shared-memory double buffer of 2 x 32 records filled by cp.async one chunk
+// ahead (collective: every lane copies one record per chunk).
+struct RecStream {
 #ifdef CACE_HOST_EMULATION
-  return p;
+  const ReqRec* g;
+  void init(const ReqRec* g_, uint32_t, ReqRec*) { g = g_; }
+  const ReqRec& get(uint32_t k) { return g[k]; }
 #else
-  return __any_sync(kFull, p);
+  const ReqRec* g;
+  uint32_t n;
+  ReqRec* buf;
+  __device__ __forceinline__ void issue(uint32_t c) {
+    const uint32_t i = c * 32 + (threadIdx.x & 31);
+    if (i < n) {
+      const char* src = reinterpret_cast<const char*>(g + i);
+      const uint32_t dst =
+          (uint32_t)__cvta_generic_to_shared(buf + ((c & 1) * 32 + (threadIdx.x & 31)));
+#pragma unroll
+      for (int b = 0; b < (int)sizeof(ReqRec); b += 16)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + b), "l"(src + b)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  __device__ __forceinline__ void init(const ReqRec* g_, uint32_t n_, ReqRec* buf_) {
+    g = g_;
+    n = n_;
+    buf = buf_;
+    issue(0);
+  }
+  __device__ __forceinline__ const ReqRec& get(uint32_t k) {
+    if ((k & 31u) == 0) {  // warp-uniform: chunk k/32 has landed; prefetch the next one
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      issue(k / 32 + 1);
+    }
+    return buf[k & 63u];
+  }
 #endif
-}
+};
 
 // Block-shared catalog columns.
 struct CatShared {
@@ -188,12 +261,17 @@ struct CatShared {
   const int* lex;     // rank of model_id under std::string <
 };
 
-// Per-lane shared-memory columns (element i at [i * stride]).
+// Per-lane shared-memory columns (element i at [i * stride]) and the lane's
+// warp-shared tables.
 struct LaneSmem {
-  float* p4f;        // [M] p4 = w1 * (tokens / normalizer), fp32 (screening)
+  float* p4f;        // [M] p2 + p4 = p2 + w1 * (tokens / normalizer), fp32 (screening)
+  double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67)
+  double* done;      // [C] |stime|: completion time of the slot's last service
   uint32_t* seq;     // [C] ServiceComplete push seq of each busy slot
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
   int stride;
+  ReqRec* rec;       // warp: record double buffer [64]
+  WinEnt* win;       // warp: window table [M]
 };
 
 // Replays one scenario (see the file comment).  shadow lanes (warp padding)
@@ -215,21 +293,30 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const double unload = sc.unload_time_s;
   const double norm = (double)sc.output_token_normalizer;
   const float rcpw = 1.0f / (float)sc.window_length;
+  // fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0
+  const float p1s = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
+  const float p1o = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
   const int st = S.stride;
   // fp32 screening is valid while every p2 + p4 is finite and moderate; the
   // event clock is finite (validated on the host) and t < 1e30 below.
+  // tbound >= |total| of every candidate (p1, p3 in [0, 1]) sets the margin.
   bool screen_ok = true;
+  float tbound = 2.0f;
   for (int mm = 0; mm < M; ++mm) {
     S.slot_of[mm * st] = 0;
-    // fp32 p2 + p4 of model mm (policy.cpp:55, 66-67), for screening only;
-    // ablated terms are 0 exactly as the reference zeroes them
+    // p2 + p4 of model mm (policy.cpp:55, 66-67): exact p4 for the fp64
+    // path, fp32 p2 + p4 for screening; ablated terms are 0 exactly as the
+    // reference zeroes them
     if (!is_lru) {
       const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[mm];
       const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[mm] / norm);
+      S.p4d[mm * st] = p4;
       S.p4f[mm * st] = (float)(p2 + p4);
       screen_ok = screen_ok && fabs(p2 + p4) <= 1e5;  // false for NaN / inf
+      if (screen_ok) tbound = fmaxf(tbound, 2.0f + fabsf((float)(p2 + p4)));
     }
   }
+  const float margin = 6e-5f + 1e-6f * (tbound + 4.0f);
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -237,17 +324,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
   }
-  RegWindow<MW> win;
-  if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M);
+  RecStream rs;
+  rs.init(tr, n, S.rec);
+  Window<MW> win;
+  if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M, tr, n, S.win);
 
-  // Slots (registers).  Bit s of `busy`: ServiceComplete pending at
-  // (stime, seq[s]); otherwise Idle with last_used = stime.  One register
-  // pair serves both: a completion sets last_used to its own event time
-  // (engine.cpp:224-229), so applying it only clears the busy bit.  The push
-  // seq (tie-break of equal completion times) lives in shared memory.
+  // Slots (registers), sign-encoded (file comment); the push seq (tie-break
+  // of equal completion times) lives in shared memory.
   int sms[C];
   double stime[C];
-  unsigned busy = 0;
 #pragma unroll
   for (int s = 0; s < C; ++s) {
     sms[s] = 0xffff;
@@ -262,78 +347,55 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
   uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
-  // Software-pipelined record stream (warp-uniform broadcast load).
-  double na = 0.0, npf = 0.0, ndc = 0.0;
-  uint32_t nnxt = 0, nmc = 0;
-  if (n > 0) load_rec(tr, na, npf, ndc, nnxt, nmc);
   for (uint32_t k = 0; k < n; ++k) {
-    const double a = na, pf = npf, dc = ndc;
-    const uint32_t nxt = nnxt, mc = nmc;
-    if (k + 1 < n) load_rec(tr + k + 1, na, npf, ndc, nnxt, nmc);
+    const ReqRec& R = rs.get(k);
+    const double a = R.arrival, pf = R.prefill, dc = R.decode;
+    const uint32_t mc = R.mc;
     const int m = (int)(mc & 0xffffu);
 
     // Head not yet pending: advance to its Arrival; completions with a
-    // smaller key idle their slots (engine.cpp:219-230).
+    // smaller key (done <= a) idle their slots (engine.cpp:219-230).
     if (!(a < cur.t)) {
+      const double na = -a;
 #pragma unroll
       for (int s = 0; s < C; ++s)
-        if ((busy >> s & 1u) && stime[s] <= a) {
-          busy &= ~(1u << s);
-        }
+        if (stime[s] >= na) stime[s] = fabs(stime[s]);
       cur = Cursor{a, 2, k};
     }
 
     // classify (engine.cpp:163-173): resident (never Loading here) -> hit
     int hs = (int)S.slot_of[m * st] - 1;
-    const unsigned idle = ~busy & ((1u << C) - 1u);
-    const bool decide = hs < 0 && occ == C && (idle & (idle - 1u)) != 0;
-
-    // Window position of every slot's model for the warp's multi-candidate
-    // decisions (collective gather): p3 = rank / w when the model's first
-    // pending request lies in the window [k, min(k + w, arrived)), else 1
-    // (policy.cpp:57-64).  Idle residents are not the head's model, so
-    // first > k.  pos[s] = rank, or -1 outside the window.
-    int pos[C];
+    int nbusy = 0;
 #pragma unroll
-    for (int s = 0; s < C; ++s) pos[s] = -1;
-    if (C > 1 && warp_win && warp_any(decide && need_win)) {
-#pragma unroll
-      for (int s = 0; s < C; ++s) {
-        uint32_t fmv, rk;
-        win.gather(slot_model(sms[s]), fmv, rk);
-        bool iw = need_win && fmv < n && fmv - k < w;
-        if (iw) iw = __ldg(&tr[fmv].arrival) < cur.t;
-        if (iw) pos[s] = (int)rk;
-      }
-    }
+    for (int s = 0; s < C; ++s) nbusy += (int)((unsigned)__double2hiint(stime[s]) >> 31);
+    const bool decide = hs < 0 && occ == C && C - nbusy >= 2;
 
     double lw = 0.0;
     const bool hit = hs >= 0;
     if (hit) {
       ++hits;
-      if (busy >> hs & 1u) {
-        // blocked until the model's own ServiceComplete
-        double td = 0.0;
-#pragma unroll
-        for (int s = 0; s < C; ++s)
-          if (s == hs) td = stime[s];
-        const uint32_t tq = S.seq[hs * st];
+      // Busy iff its ServiceComplete key (td, 1, tq) is after the cursor
+      // (the sign of stime[hs] says the same; the shadow avoids a dynamic
+      // register read).
+      const double td = S.done[hs * st];
+      const uint32_t tq = S.seq[hs * st];
+      if (td > cur.t || (td == cur.t && (cur.kind == 0 || (cur.kind == 1 && tq > cur.seq)))) {
+        // Busy: blocked until the model's own ServiceComplete (td, 1, tq).
+        // Completions with key <= it become Idle: done < td, and equal
+        // times break ties on the push seq.
         cur = Cursor{td, 1, tq};
-        // completions with key <= (td, 1, tq); equal times (rare) break ties
-        // on the push seq.
-        unsigned done_m = 1u << hs, eq = 0u;
+        const double ntd = -td;
+        bool tie = false;
 #pragma unroll
         for (int s = 0; s < C; ++s) {
-          done_m |= (stime[s] < td) ? (1u << s) : 0u;
-          eq |= (stime[s] == td && s != hs) ? (1u << s) : 0u;
+          if (stime[s] > ntd) stime[s] = fabs(stime[s]);
+          tie |= s != hs && stime[s] == ntd;
         }
-        eq &= busy;
-        while (eq) {
-          const int s = __ffs(eq) - 1;
-          eq &= eq - 1u;
-          if (S.seq[s * st] <= tq) done_m |= 1u << s;
+        if (tie) {
+#pragma unroll
+          for (int s = 0; s < C; ++s)
+            if (s != hs && stime[s] == ntd && S.seq[s * st] <= tq) stime[s] = td;
         }
-        busy &= ~done_m;
       }
     } else {
       int v;
@@ -341,23 +403,24 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
       } else {
-        if (idle == 0) {
+        if (nbusy == C) {
           // every resident busy: the next event is the min-key
           // ServiceComplete, whose slot is then the only Idle one.
           int s1 = 0;
-          double t1 = stime[0];
+          double t1 = stime[0];  // = -done: max t1 = min done
 #pragma unroll
           for (int s = 1; s < C; ++s)
-            if (stime[s] < t1 || (stime[s] == t1 && S.seq[s * st] < S.seq[s1 * st])) {
+            if (stime[s] > t1 || (stime[s] == t1 && S.seq[s * st] < S.seq[s1 * st])) {
               s1 = s;
               t1 = stime[s];
             }
-          const uint32_t q1 = S.seq[s1 * st];
-          busy &= ~(1u << s1);
-          cur = Cursor{t1, 1, q1};
+          cur = Cursor{-t1, 1, S.seq[s1 * st]};
           v = s1;
         } else if (!decide) {
-          v = __ffs(idle) - 1;  // exactly one candidate
+          v = 0;  // exactly one candidate
+#pragma unroll
+          for (int s = 1; s < C; ++s)
+            if (is_idle(stime[s])) v = s;
         } else {
           // ---- eviction decision among >= 2 idle residents ----------
           const double now = cur.t;
@@ -370,7 +433,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
             for (int s = 0; s < C; ++s) {
               const int lx = slot_lex(sms[s]);
-              if ((idle >> s & 1u) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
+              if (is_idle(stime[s]) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
                 f = s;
                 flu = stime[s];
                 flex = lx;
@@ -378,45 +441,41 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             }
             return f;
           };
+          // p3 (policy.cpp:57-64): rank / w when the model's first pending
+          // request lies in the window [k, min(k + w, arrived)), else 1.
+          // Idle residents are not the head's model, so first > k.
           if (is_lru) {
             v = sorted_first();
           } else {
             // fp32 screening with a rigorous bound: if one candidate's
             // approximate total beats every other by more than the bound it
-            // is the exact arg-max.  |dL| <= 2.3e-5 (3-ulp __logf, ln t < 70)
-            // propagates with Lipschitz constant 1 through 1/(1+L);
-            // __fdividef, rank*(1/w), p4 = w1*tok*(1/norm), the term
-            // conversions and three fp32 sums add <= 2^-21 (|T| + 4).  The
-            // margin is twice the worst case.
-            float best = -INFINITY, second = -INFINITY, tmax = 0.0f;
-            int bs = -1;
-            bool exact = !screen_ok;
+            // is the exact arg-max.  |dL| <= 2.3e-5 (lg2.approx, ln t < 70)
+            // propagates with Lipschitz constant 1 through 1/(1+L); the
+            // approximate reciprocal, rank*(1/w), p4 = w1*tok*(1/norm), the
+            // term conversions and three fp32 sums add <= 2^-21 (|T| + 4).
+            // The margin is twice the worst case.
+            float best = -INFINITY, second = -INFINITY;
+            int bs = 0;
+            const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
               const int ms = slot_model(sms[s]);
-              float p1 = 0.0f;
-              if (variant != CACE_MINUS_P1) {
-                const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
-                const float p1v = __fdividef(1.0f, 1.0f + __logf(t));
-                p1 = verbatim ? p1v : 1.0f - p1v;
+              const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
+              const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
+              const float p1 = fmaf(p1s, p1v, p1o);
+              float p3 = 0.0f;
+              if (need_win) {
+                const WinEnt e = win.gather(ms);
+                p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
               }
-              const float p3 =
-                  variant == CACE_MINUS_P3 ? 0.0f : (pos[s] >= 0 ? (float)pos[s] * rcpw : 1.0f);
-              const float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
-              if (idle >> s & 1u) {
-                tmax = fmaxf(tmax, fabsf(T));
-                if (T > best) {
-                  second = best;
-                  best = T;
-                  bs = s;
-                } else if (T > second) {
-                  second = T;
-                }
-              }
+              float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
+              T = is_idle(stime[s]) ? T : -INFINITY;
+              bs = T > best ? s : bs;
+              second = fmaxf(second, fminf(best, T));
+              best = fmaxf(best, T);
             }
-            exact |= !(best - second > 6e-5f + 1e-6f * (tmax + 4.0f));
             v = bs;
-            if (exact) {
+            if (!screen_ok || !(best - second > margin)) {
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
               // strict max in (last_used, model_id) order"
               // (policy.cpp:92-113), bit-identical to the reference; taken on
@@ -430,7 +489,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               int blex = 0, bv = -1;
 #pragma unroll
               for (int s = 0; s < C; ++s) {
-                if (!(idle >> s & 1u)) continue;
+                if (!is_idle(stime[s])) continue;
                 const int ms = slot_model(sms[s]);
                 const int lx = slot_lex(sms[s]);
                 double p1 = 0.0;
@@ -443,9 +502,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                   p1 = verbatim ? p1v : 1.0 - p1v;
                 }
                 const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
-                const double p3 =
-                    variant == CACE_MINUS_P3 ? 0.0 : (pos[s] >= 0 ? (double)pos[s] / wd : 1.0);
-                const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm);
+                double p3 = 0.0;
+                if (variant != CACE_MINUS_P3) {
+                  const WinEnt e = win.gather(ms);
+                  p3 = (e.f - k < w && e.fa < now) ? (double)e.r / wd : 1.0;
+                }
+                const double p4 = S.p4d[ms * st];
                 const double T = ((p1 + p2) + p3) + p4;
                 if (s == f) f_nan = T != T;
                 if (T == T && (bv < 0 || T > bt ||
@@ -487,11 +549,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       for (int s = 0; s < C; ++s)
         if (s == v) sms[s] = word;
       S.slot_of[m * st] = (uint8_t)(v + 1);
+      const double nr = -r;
 #pragma unroll
       for (int s = 0; s < C; ++s)
-        if ((busy >> s & 1u) && stime[s] < r) {
-          busy &= ~(1u << s);
-        }
+        if (stime[s] > nr) stime[s] = fabs(stime[s]);
       cur = Cursor{r, 0, 0};
       hs = v;
     }
@@ -504,18 +565,18 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const double done = (now + pf) + dc;
 #pragma unroll
     for (int s = 0; s < C; ++s)
-      if (s == hs) stime[s] = done;
+      if (s == hs) stime[s] = -done;
+    S.done[hs * st] = done;
     S.seq[hs * st] = seqc;
-    busy |= 1u << hs;
     ++seqc;
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
-      mttft = ttft > mttft ? ttft : mttft;
+      mttft = fmax(mttft, ttft);  // no NaN: finite event times
     } else {
       se2e += e2e;
-      me2e = e2e > me2e ? e2e : me2e;
+      me2e = fmax(me2e, e2e);
     }
-    ho = hmix(ho, dbits(ttft) ^ swap32(dbits(e2e)) ^ (hit ? 0ull : 1ull));
+    ho = hmix(ho, dbits(ttft) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0) {
       const int64_t o = doff + P.perm[base + k];
       if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
@@ -526,7 +587,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (P.dump.ttft) P.dump.ttft[o] = ttft;
       if (P.dump.e2e) P.dump.e2e[o] = e2e;
     }
-    if (C > 1 && warp_win) win.advance(m, nxt);  // the head leaves the window (collective)
+    // the head leaves the window (collective)
+    if (C > 1 && warp_win) win.advance(m, R.nxt, R.nxa);
   }
 
   if (shadow) return;
@@ -556,8 +618,21 @@ constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 regi
 #ifndef CACE_HOST_EMULATION
 constexpr int LANE_BLOCK = 128;
 #ifndef CACE_LANE_MIN_BLOCKS
-#define CACE_LANE_MIN_BLOCKS 4  // <= 128 registers: 4 blocks (16 warps) per SM; measured +4% vs uncapped
+#define CACE_LANE_MIN_BLOCKS 4  // <= 128 registers: 4 blocks (16 warps) per SM
 #endif
+
+// Dynamic shared memory of one lane block: catalog columns, per-lane columns
+// [M or C][LANE_BLOCK], then per warp the record double buffer and the
+// window table.
+inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
+inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
+  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + C * 4 + M);
+}
+inline __host__ __device__ size_t lane_smem_warp(int M) { return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt); }
+inline size_t lane_smem_bytes(int M, int C) {
+  const size_t a = (((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
+  return a + (LANE_BLOCK / 32) * lane_smem_warp(M);
+}
 
 template <int C, int MW, bool DUMP>
 __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_kernel(ReplayParams P) {
@@ -569,9 +644,17 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   float* s_p2f = reinterpret_cast<float*>(s_tok + M);
   float* s_tokf = s_p2f + M;
   int* s_lex = reinterpret_cast<int*>(s_tokf + M);
-  float* l_p4f = reinterpret_cast<float*>(s_lex + M);                   // [M][LANE_BLOCK]
+  // per-lane columns: 8-B ones first (M * 36 B of catalog keeps 4-B alignment only)
+  double* l_p4d = reinterpret_cast<double*>(smem + ((lane_smem_cat(M) + 7) & ~(size_t)7));  // [M][LB]
+  double* l_done = l_p4d + (size_t)M * LANE_BLOCK;                                          // [C][LB]
+  float* l_p4f = reinterpret_cast<float*>(l_done + (size_t)C * LANE_BLOCK);                // [M][LB]
   uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_p4f + (size_t)M * LANE_BLOCK);  // [C][LANE_BLOCK]
   uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_seq + (size_t)C * LANE_BLOCK);   // [M][LANE_BLOCK]
+  unsigned char* wbase =
+      smem + ((((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
+      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M);
+  ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
+  WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
@@ -582,7 +665,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   }
   __syncthreads();
   const int64_t gi = P.seg_begin + (int64_t)blockIdx.x * LANE_BLOCK + threadIdx.x;
-  if (gi >= P.seg_end) return;  // the plan pads groups to whole warps
+  if (gi >= P.seg_end) return;  // whole warps: the plan pads groups to whole warps
   const uint64_t e = (uint64_t)P.order[gi];
   const bool shadow = (e & kShadowBit) != 0;
   const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
@@ -590,12 +673,9 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
   const bool warp_win = __any_sync(kFull, need_win);
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
-  const LaneSmem S{l_p4f + threadIdx.x, l_seq + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK};
+  const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x,
+                   l_seq + threadIdx.x,  l_slot + threadIdx.x, LANE_BLOCK, w_rec, w_win};
   replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);
-}
-
-inline size_t lane_smem_bytes(int M, int C) {
-  return (size_t)M * (3 * 8 + 2 * 4 + 4) + (size_t)LANE_BLOCK * (M * 4 + C * 4 + M);
 }
 #endif  // CACE_HOST_EMULATION
 

@@ -9,15 +9,19 @@ namespace cace {
 
 enum : int { ST_IDLE = 0, ST_BUSY = 1, ST_LOADING = 2 };
 
-// One request in replay (sorted) order.  32 B = one sector: a lane advancing
-// its queue head fetches exactly one sector (two 128-bit loads).
-struct alignas(32) ReqRec {
+// One request in replay (sorted) order, 48 B (three 16-B cp.async chunks).
+// The first 32 B are what a replay step reads; `nxa` feeds the lookahead
+// window (arrival time of the next request for the same model).
+struct alignas(16) ReqRec {
   double arrival;  // Request::arrival_time_s
   double prefill;  // service_times(): prompt / prefill_rate   (engine.cpp:21-22)
   double decode;   // service_times(): max(out,1) / decode_rate (engine.cpp:23-24)
   uint32_t nxt;    // next sorted index with the same model (n if none)
   uint32_t mc;     // model | task_class << 16
+  double nxa;      // arrival of request nxt (+inf if none)
+  double pad;
 };
+static_assert(sizeof(ReqRec) == 48, "ReqRec layout");
 
 struct DevCatalog {
   int M;

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
       se2e += e2e;
       me2e = e2e > me2e ? e2e : me2e;
     }
-    ho = hmix(ho, dbits(ttft) ^ swap32(dbits(e2e)) ^ (hit ? 0ull : 1ull));
+    ho = hmix(ho, dbits(ttft) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0 && lane == 0) {
       const int64_t o = doff + P.perm[base + k];
       if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;

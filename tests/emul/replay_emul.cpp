@@ -27,6 +27,8 @@ static inline double __hiloint2double(int hi, int lo) {
   return d;
 }
 static inline long long __double_as_longlong(double d) { long long u; std::memcpy(&u, &d, 8); return u; }
+static inline int __double2hiint(double d) { return (int)(__double_as_longlong(d) >> 32); }
+static inline unsigned __float_as_uint(float f) { unsigned u; std::memcpy(&u, &f, 4); return u; }
 #define __logf(x) logf(x)
 static inline float __fdividef(float a, float b) { return a / b; }
 static inline int __ffs(unsigned x) { return __builtin_ffs((int)x); }
@@ -44,9 +46,10 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
   std::vector<float> p4f(P.cat.M);
+  std::vector<double> p4d(P.cat.M), done(C);
   std::vector<uint32_t> seq(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), seq.data(), slot_of.data(), 1};
+  const LaneSmem S{p4f.data(), p4d.data(), done.data(), seq.data(), slot_of.data(), 1, nullptr, nullptr};
   replay_scenario<C, 2, D>(P, i, false, need_win, K, S);
 }
 
