@@ -42,11 +42,14 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = OUT) -> str:
+    if out != OUT:
+        return _build_to(out, verbose)
     if not force and up_to_date():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SOURCES]
+    extra = os.environ.get("CACE_NVCC_EXTRA", "").split()  # experiments, e.g. -DCACE_LANE_MIN_BLOCKS=5
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", OUT + ".tmp", *SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
@@ -54,5 +57,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def _build_to(out: str, verbose: bool) -> str:
+    extra = os.environ.get("CACE_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", out, *SOURCES]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    print(build(force="--force" in sys.argv, verbose=True, out=os.path.abspath(args[0]) if args else OUT))

@@ -119,6 +119,18 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 #endif
 
+// Exact fp64 P1 of eviction_score (policy.cpp:50-53) with the glibc log.
+// Out of line: one copy serves every unrolled candidate of the rare exact
+// path, and its temporaries do not add to the replay loop's register peak.
+__device__ __noinline__ double exact_p1(double now, double last_used, bool verbatim, int log_variant,
+                                        const double* tab, const double* tab2) {
+  const double d = now - last_used;
+  const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
+  const double lg = t == 1.0 ? 0.0 : cace_glibc_log(t, log_variant, tab, tab2);
+  const double p1v = 1.0 / (1.0 + lg);
+  return verbatim ? p1v : 1.0 - p1v;
+}
+
 // Per-warp window table entry: first pending index of the model, its rank
 // among the models' first occurrences (as a float: an exact small integer),
 // and that request's arrival time (+inf when the model has no pending
@@ -492,15 +504,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 if (!is_idle(stime[s])) continue;
                 const int ms = slot_model(sms[s]);
                 const int lx = slot_lex(sms[s]);
-                double p1 = 0.0;
-                if (variant != CACE_MINUS_P1) {
-                  const double d = now - stime[s];
-                  const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
-                  const double lg =
-                      t == 1.0 ? 0.0 : cace_glibc_log(t, P.log_variant, P.log_tab, P.log_tab2);
-                  const double p1v = 1.0 / (1.0 + lg);
-                  p1 = verbatim ? p1v : 1.0 - p1v;
-                }
+                const double p1 = variant == CACE_MINUS_P1
+                                      ? 0.0
+                                      : exact_p1(now, stime[s], verbatim, P.log_variant, P.log_tab, P.log_tab2);
                 const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
                 double p3 = 0.0;
                 if (variant != CACE_MINUS_P3) {
@@ -571,10 +577,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     ++seqc;
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
-      mttft = fmax(mttft, ttft);  // no NaN: finite event times
+      mttft = ttft > mttft ? ttft : mttft;
     } else {
       se2e += e2e;
-      me2e = fmax(me2e, e2e);
+      me2e = e2e > me2e ? e2e : me2e;
     }
     ho = hmix(ho, dbits(ttft) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0) {

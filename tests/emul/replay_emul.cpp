@@ -17,6 +17,7 @@
 #define __host__
 #define __global__
 #define __forceinline__ inline
+#define __noinline__
 #define __launch_bounds__(...)
 struct uint4 { unsigned x, y, z, w; };
 template <typename T> static inline T __ldg(const T* p) { return *p; }
