@@ -285,6 +285,17 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     }
     k = j;
   }
+  // Launch the most expensive segments first: the block scheduler fills the
+  // GPU in launch order, so cheap segments then backfill the tail of the
+  // long ones.  Replay cost grows with the number of eviction candidates,
+  // ~min(C, M - 1) per decision; C >= M never evicts.
+  const int M = e->cat.M;
+  auto seg_cost = [&](const cace_engine::Seg& g) {
+    const double per = g.warp ? 64.0 : (g.C >= M ? 2.0 : (double)std::min(g.C, M - 1));
+    return per * (double)(g.e - g.b);
+  };
+  std::stable_sort(e->segs.begin(), e->segs.end(),
+                   [&](const cace_engine::Seg& x, const cace_engine::Seg& y) { return seg_cost(x) > seg_cost(y); });
   e->d_order.upload(order.data(), order.size(), e->stream);
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
   e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);

@@ -228,7 +228,7 @@ struct RecStream {
 #ifdef CACE_HOST_EMULATION
   const ReqRec* g;
   void init(const ReqRec* g_, uint32_t, ReqRec*) { g = g_; }
-  const ReqRec& get(uint32_t k) { return g[k]; }
+  const ReqRec* chunk(uint32_t c) { return g + (size_t)c * 32; }
 #else
   const ReqRec* g;
   uint32_t n;
@@ -252,13 +252,13 @@ struct RecStream {
     buf = buf_;
     issue(0);
   }
-  __device__ __forceinline__ const ReqRec& get(uint32_t k) {
-    if ((k & 31u) == 0) {  // warp-uniform: chunk k/32 has landed; prefetch the next one
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
-      issue(k / 32 + 1);
-    }
-    return buf[k & 63u];
+  // Collective: records [32c, 32c + 32) once chunk c has landed; prefetches
+  // chunk c + 1 into the other half.
+  __device__ __forceinline__ const ReqRec* chunk(uint32_t c) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    issue(c + 1);
+    return buf + (c & 1) * 32;
   }
 #endif
 };
@@ -359,8 +359,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
   uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
 
-  for (uint32_t k = 0; k < n; ++k) {
-    const ReqRec& R = rs.get(k);
+  for (uint32_t c = 0, k = 0; k < n; ++c) {
+  const ReqRec* const cb = rs.chunk(c);
+  const uint32_t kend = n - k < 32 ? n : k + 32;
+  for (const ReqRec* rp = cb; k < kend; ++k, ++rp) {
+    const ReqRec& R = *rp;
     const double a = R.arrival, pf = R.prefill, dc = R.decode;
     const uint32_t mc = R.mc;
     const int m = (int)(mc & 0xffffu);
@@ -595,6 +598,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     }
     // the head leaves the window (collective)
     if (C > 1 && warp_win) win.advance(m, R.nxt, R.nxa);
+  }
   }
 
   if (shadow) return;
