@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -26,6 +28,19 @@ namespace {
 const double kLogTab[256] = CACE_GLIBC_LOG_TAB;
 const double kLogTab2[256] = CACE_GLIBC_LOG_TAB2;
 
+// CACE_TIMING=1: host phase timings of cace_replay_batch on stderr.
+struct PhaseTimer {
+  bool on = std::getenv("CACE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "cace_timing %-16s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void put_msg(char* msg, size_t cap, const std::string& s) {
   if (!msg || cap == 0) return;
   const size_t k = std::min(cap - 1, s.size());
@@ -45,30 +60,85 @@ struct CudaFail {
       throw CudaFail{CACE_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
   } while (0)
 
-// Device buffer owned by RAII.
+// Keep freed memory in the device's default pool (stream-ordered
+// allocator): repeated engine builds / batch calls then reuse it instead of
+// paying cudaMalloc/cudaFree of hundreds of MB every call.
+void retain_pool(int dev) {
+  static std::mutex mu;
+  static std::vector<bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)done.size() <= dev) done.resize(dev + 1, false);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[dev] = true;
+}
+
+// Device buffer owned by RAII, allocated and freed in order on one stream
+// (the owner synchronises that stream, or joins every stream that used the
+// buffer into it, before the buffer is released).
 template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = 0;
   }
-  void alloc(size_t k) {
+  void alloc(size_t k, cudaStream_t s) {
     release();
     n = k;
-    if (k) CK(cudaMalloc(&p, k * sizeof(T)));
+    st = s;
+    if (k) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), k * sizeof(T), s));
   }
   void upload(const T* h, size_t k, cudaStream_t s) {
-    alloc(k);
+    alloc(k, s);
     if (k) CK(cudaMemcpyAsync(p, h, k * sizeof(T), cudaMemcpyHostToDevice, s));
   }
 };
+
+// Process-wide pinned staging area for the trace records: the layout is
+// built straight into page-locked memory (no page faults after the first
+// use, DMA upload).  One engine build uses it at a time; a concurrent build
+// falls back to pageable memory.
+struct PinnedArena {
+  std::mutex mu;
+  void* p = nullptr;
+  size_t cap = 0;
+  bool busy = false;
+  void* acquire(size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (busy) return nullptr;
+    if (cap < bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return nullptr;
+      }
+      cap = bytes;
+    }
+    busy = true;
+    return p;
+  }
+  void release() {
+    std::lock_guard<std::mutex> lk(mu);
+    busy = false;
+  }
+};
+PinnedArena g_arena;
 
 int g_probe = -2;
 std::mutex g_probe_mu;
@@ -122,6 +192,7 @@ void require_device(const cace_opts_t* o) {
   const int dev = o ? o->device : 0;
   if (dev < 0 || dev >= n) throw Invalid{CACE_E_INVALID, "cace: device ordinal out of range"};
   CK(cudaSetDevice(dev));
+  retain_pool(dev);
 }
 
 // Host catalog + its device columns.
@@ -196,11 +267,26 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
     e->joins.push_back(ev);
   }
   CK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+  PhaseTimer pt;
   e->cat.load(catalog);
+  struct ArenaGuard {
+    bool held = false;
+    ~ArenaGuard() {
+      if (held) g_arena.release();
+    }
+  } guard;
+  if (n_traces > 0 && traces) {
+    const int64_t N = layout_requests(traces, n_traces);
+    if (N >= (1 << 16)) {
+      e->lay.ext_rec = static_cast<ReqRec*>(g_arena.acquire((size_t)N * sizeof(ReqRec)));
+      guard.held = e->lay.ext_rec != nullptr;
+    }
+  }
   build_layout(e->cat, traces, n_traces, e->lay);
+  pt.mark("  layout");
   cudaStream_t s = e->stream;
   e->cat.upload(s);
-  e->d_rec.upload(e->lay.rec.data(), e->lay.rec.size(), s);
+  e->d_rec.upload(e->lay.records(), (size_t)e->lay.off[e->lay.T], s);
   e->d_off.upload(e->lay.off.data(), e->lay.off.size(), s);
   e->d_first0.upload(e->lay.first0.data(), e->lay.first0.size(), s);
   e->d_perm.upload(e->lay.perm.data(), e->lay.perm.size(), s);
@@ -208,12 +294,15 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
   e->d_tab.upload(kLogTab, 256, s);
   e->d_tab2.upload(kLogTab2, 256, s);
   CK(cudaStreamSynchronize(s));
-  std::vector<ReqRec>().swap(e->lay.rec);  // device copy is authoritative
+  pt.mark("  upload");
+  decltype(e->lay.rec)().swap(e->lay.rec);  // device copy is authoritative
+  e->lay.ext_rec = nullptr;
   std::vector<uint32_t>().swap(e->lay.perm);
 }
 
 void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   if (n < 0 || (n > 0 && !sc)) throw Invalid{CACE_E_INVALID, "cace: bad scenario array"};
+  PhaseTimer pt;
   e->segs.clear();
   e->bad_idx.clear();
   e->bad_code.clear();
@@ -230,6 +319,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
       ok.push_back(i);
     }
   }
+  pt.mark("  precheck");
   auto capof = [&](int64_t i) {
     return (int)((int64_t)sc[i].num_accelerators * sc[i].models_per_accelerator);
   };
@@ -249,16 +339,37 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     return use_warp(i) ? 1000 + (C <= 32 ? 1 : 2) : C;
   };
   // Coherent warps: segment, then trace, then the control-flow shaping
-  // policy fields.
-  std::stable_sort(ok.begin(), ok.end(), [&](int64_t a, int64_t b) {
-    const cace_scenario_t &x = sc[a], &y = sc[b];
-    const int ka = key(a), kb = key(b);
-    if (ka != kb) return ka < kb;
-    if (x.trace != y.trace) return x.trace < y.trace;
-    if (x.variant != y.variant) return x.variant < y.variant;
-    if (x.window_length != y.window_length) return x.window_length < y.window_length;
-    return x.p1_mode < y.p1_mode;
-  });
+  // policy fields.  Stable counting sort by segment (O(S)), then each
+  // segment is sorted by (trace, variant, p1_mode, window) unless it already
+  // is (the common case for generated sweeps).
+  {
+    std::vector<int> kv(ok.size());
+    int kmax = 0;
+    for (size_t j = 0; j < ok.size(); ++j) {
+      const int K = key(ok[j]);
+      kv[j] = K >= 1000 ? kMaxLaneC + (K - 1000) : K;  // dense: 1..16 lane, 17..18 warp
+      kmax = std::max(kmax, kv[j]);
+    }
+    std::vector<int64_t> cnt(kmax + 2, 0);
+    for (int k : kv) ++cnt[k + 1];
+    for (int k = 1; k <= kmax + 1; ++k) cnt[k] += cnt[k - 1];
+    std::vector<int64_t> by_seg(ok.size());
+    std::vector<int64_t> start(cnt.begin(), cnt.end());
+    for (size_t j = 0; j < ok.size(); ++j) by_seg[start[kv[j]]++] = ok[j];
+    auto lt = [&](int64_t a, int64_t b) {
+      const cace_scenario_t &x = sc[a], &y = sc[b];
+      if (x.trace != y.trace) return x.trace < y.trace;
+      if (x.variant != y.variant) return x.variant < y.variant;
+      if (x.p1_mode != y.p1_mode) return x.p1_mode < y.p1_mode;
+      return x.window_length < y.window_length;
+    };
+    for (int k = 0; k <= kmax; ++k) {
+      auto b = by_seg.begin() + cnt[k], e2 = by_seg.begin() + cnt[k + 1];
+      if (!std::is_sorted(b, e2, lt)) std::stable_sort(b, e2, lt);
+    }
+    ok.swap(by_seg);
+  }
+  pt.mark("  sort");
   // Lane segments: every (capacity, trace) group is padded to a whole number
   // of warps with shadow lanes (copies of the group's first scenario that
   // write nothing) so each warp is trace-uniform and walks its trace in
@@ -285,6 +396,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     }
     k = j;
   }
+  pt.mark("  order");
   // Launch the most expensive segments first: the block scheduler fills the
   // GPU in launch order, so cheap segments then backfill the tail of the
   // long ones.  Replay cost grows with the number of eviction candidates,
@@ -461,6 +573,22 @@ void cace_engine_destroy(cace_engine* e) {
   }
   for (auto ev : e->joins) cudaEventDestroy(ev);
   if (e->fork) cudaEventDestroy(e->fork);
+  // device buffers go back to the pool in order on the engine stream, which
+  // must still exist
+  e->cat.d_lt.release();
+  e->cat.d_p2.release();
+  e->cat.d_tok.release();
+  e->cat.d_lex.release();
+  e->d_rec.release();
+  e->d_off.release();
+  e->d_first0.release();
+  e->d_perm.release();
+  e->d_ncomp.release();
+  e->d_tab.release();
+  e->d_tab2.release();
+  e->d_order.release();
+  e->d_bad_idx.release();
+  e->d_bad_code.release();
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -500,16 +628,19 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
                           cace_summary_t* summaries, const cace_dump_t* dump,
                           const cace_opts_t* opts, char* msg, size_t msg_cap) {
   cace_engine* e = nullptr;
+  PhaseTimer pt;
   int32_t rc = cace_engine_create(catalog, traces, n_traces, opts, &e, msg, msg_cap);
   if (rc != CACE_OK) return rc;
+  pt.mark("engine_create");
   rc = guarded(msg, msg_cap, [&]() -> int32_t {
     if (n_scenarios > 0 && !summaries) throw Invalid{CACE_E_INVALID, "cace: summaries is NULL"};
     plan(e, scenarios, n_scenarios);
+    pt.mark("plan");
     cudaStream_t s = e->stream;
     DBuf<cace_scenario_t> d_sc;
     d_sc.upload(scenarios, n_scenarios, s);
     DBuf<cace_summary_t> d_out;
-    d_out.alloc(n_scenarios);
+    d_out.alloc(n_scenarios, s);
     // Optional full dump.
     DumpDev dd{};
     DBuf<int32_t> d_slot;
@@ -536,11 +667,11 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       dd.dump_off = d_doff.p;
       auto mk = [&](DBuf<double>& b, double* h) -> double* {
         if (!h) return nullptr;
-        b.alloc(total);
+        b.alloc(total, s);
         return b.p;
       };
       if (dump->cold_start) {
-        d_cold.alloc(total);
+        d_cold.alloc(total, s);
         dd.cold = d_cold.p;
       }
       dd.queue_wait = mk(d_qw, dump->queue_wait_s);
@@ -551,18 +682,26 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       dd.e2e = mk(d_ee, dump->e2e_s);
       dd.evict_cap = dump->evict_cap;
       if (dump->evict_model && dump->evict_cap > 0) {
-        d_em.alloc((size_t)nd * dump->evict_cap);
+        d_em.alloc((size_t)nd * dump->evict_cap, s);
         dd.evict_model = d_em.p;
       }
       if (dump->evict_clock && dump->evict_cap > 0) {
-        d_ec.alloc((size_t)nd * dump->evict_cap);
+        d_ec.alloc((size_t)nd * dump->evict_cap, s);
         dd.evict_clock = d_ec.p;
       }
-      d_nev.alloc(nd);
+      d_nev.alloc(nd, s);
       CK(cudaMemsetAsync(d_nev.p, 0, nd * sizeof(int64_t), s));
       dd.n_evict = d_nev.p;
     }
+    if (pt.on) {
+      CK(cudaStreamSynchronize(s));
+      pt.mark("upload_scen");
+    }
     replay(e, d_sc.p, n_scenarios, d_out.p, dd, s);
+    if (pt.on) {
+      CK(cudaStreamSynchronize(s));
+      pt.mark("replay");
+    }
     if (n_scenarios > 0)
       CK(cudaMemcpyAsync(summaries, d_out.p, n_scenarios * sizeof(cace_summary_t),
                          cudaMemcpyDeviceToHost, s));
@@ -582,6 +721,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       back(dump->n_evict, d_nev.p, (size_t)nd * 8);
     }
     CK(cudaStreamSynchronize(s));
+    pt.mark("download");
     for (int64_t i = 0; i < n_scenarios; ++i) {
       if (summaries[i].status != CACE_OK) {
         put_msg(msg, msg_cap, status_text(e->cat, summaries[i].status));
@@ -591,6 +731,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
     return CACE_OK;
   });
   cace_engine_destroy(e);
+  pt.mark("destroy");
   return rc;
 }
 
@@ -626,8 +767,8 @@ int32_t cace_select_victim_batch(const cace_catalog_t* catalog, int64_t n_instan
     d_pol.upload(policy, n_instances, s);
     d_tab.upload(kLogTab, 256, s);
     d_tab2.upload(kLogTab2, 256, s);
-    d_v.alloc(n_instances);
-    d_st.alloc(n_instances);
+    d_v.alloc(n_instances, s);
+    d_st.alloc(n_instances, s);
     select_victim_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
         cat.dev(), n_instances, max_entries, d_ne.p, d_em.p, d_lu.p, d_busy.p, max_window, d_nw.p,
         d_wm.p, d_clk.p, d_pol.p, d_tab.p, d_tab2.p, resolve_log_variant(opts), d_v.p, d_st.p);
@@ -674,8 +815,8 @@ int32_t cace_eviction_score_batch(const cace_catalog_t* catalog, int64_t n_insta
     d_pol.upload(policy, n_instances, s);
     d_tab.upload(kLogTab, 256, s);
     d_tab2.upload(kLogTab2, 256, s);
-    d_out.alloc((size_t)n_instances * 5);
-    d_st.alloc(n_instances);
+    d_out.alloc((size_t)n_instances * 5, s);
+    d_st.alloc(n_instances, s);
     eviction_score_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
         cat.dev(), n_instances, d_m.p, d_lu.p, max_window, d_nw.p, d_wm.p, d_clk.p, d_pol.p,
         d_tab.p, d_tab2.p, resolve_log_variant(opts), d_out.p, d_st.p);
@@ -712,8 +853,8 @@ int32_t cace_dedup_window_batch(int64_t n_instances, int32_t max_pending, const 
     d_np.upload(n_pending, n_instances, s);
     if (NP) d_pm.upload(pending_models, NP, s);
     d_len.upload(length, n_instances, s);
-    d_om.alloc(NP ? NP : 1);
-    d_no.alloc(n_instances);
+    d_om.alloc(NP ? NP : 1, s);
+    d_no.alloc(n_instances, s);
     dedup_window_kernel<<<(unsigned)((n_instances + 127) / 128), 128, 0, s>>>(
         n_instances, max_pending, d_np.p, d_pm.p, d_len.p, d_om.p, d_no.p);
     CK(cudaGetLastError());
@@ -749,8 +890,8 @@ int32_t cace_service_times_batch(const cace_catalog_t* catalog, int64_t n, const
     d_m.upload(model, n, s);
     d_p.upload(prompt_tokens, n, s);
     d_o.upload(output_tokens, n, s);
-    d_pf.alloc(n);
-    d_dc.alloc(n);
+    d_pf.alloc(n, s);
+    d_dc.alloc(n, s);
     service_times_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, d_m.p, d_p.p, d_o.p, d_pr.p,
                                                                       d_dr.p, d_pf.p, d_dc.p);
     CK(cudaGetLastError());
@@ -770,7 +911,7 @@ int32_t cace_log_selftest(const double* x, int64_t n, int32_t log_variant, doubl
     const int v = log_variant >= 0 ? log_variant : resolve_log_variant(opts);
     DBuf<double> d_x, d_o, d_tab, d_tab2;
     d_x.upload(x, n, s);
-    d_o.alloc(n);
+    d_o.alloc(n, s);
     d_tab.upload(kLogTab, 256, s);
     d_tab2.upload(kLogTab2, 256, s);
     log_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, d_x.p, v, d_tab.p, d_tab2.p, d_o.p);

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cace_gpu.h"
@@ -69,16 +70,45 @@ struct HostCatalog {
   bool bad_rates(int m) const { return pr[m] <= 0 || dr[m] <= 0; }  // engine.cpp:17
 };
 
+// std::allocator that default-initialises (no zero fill of the large
+// record array: every element is written by build_layout).
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  DefaultInitAlloc() = default;
+  template <class U>
+  DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+
 // Replay-order layout of all traces, concatenated.
 struct HostLayout {
   int T = 0;
   std::vector<int64_t> off;        // [T+1]
-  std::vector<ReqRec> rec;         // [N] sorted by (arrival, index)
+  std::vector<ReqRec, DefaultInitAlloc<ReqRec>> rec;  // [N] sorted by (arrival, index)
+  ReqRec* ext_rec = nullptr;  // if set (>= N records): records are written here instead of `rec`
+  ReqRec* records() { return ext_rec ? ext_rec : rec.data(); }
   std::vector<uint32_t> perm;      // [N] sorted position -> caller's request index
   std::vector<uint32_t> first0;    // [T][M] first sorted index of each model (n if absent)
   std::vector<int32_t> bad_model;  // [T] model of the first request with bad rates, or -1
   std::vector<uint32_t> ncomp;     // [T] completion-class requests
 };
+
+inline int64_t layout_requests(const cace_trace_t* traces, int32_t n_traces) {
+  int64_t N = 0;
+  for (int t = 0; t < n_traces; ++t) N += std::max<int64_t>(0, traces[t].n_requests);
+  return N;
+}
 
 inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int32_t n_traces,
                          HostLayout& L) {
@@ -92,13 +122,20 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
     L.off[t + 1] = L.off[t] + traces[t].n_requests;
   }
   const int64_t N = L.off[n_traces];
-  L.rec.assign(N, ReqRec{});
-  L.perm.assign(N, 0);
+  L.rec.clear();
+  if (!L.ext_rec) L.rec.resize(N);
+  ReqRec* const rec = L.records();
+  L.perm.resize(N);
   L.first0.assign((size_t)n_traces * M, 0);
   L.bad_model.assign(n_traces, -1);
   L.ncomp.assign(n_traces, 0);
-  std::vector<uint32_t> last(M);
-  for (int t = 0; t < n_traces; ++t) {
+  // Traces are independent: lay them out on several host threads; the error
+  // reported is the one of the lowest-numbered failing trace (as a serial
+  // pass would report).
+  std::vector<double> worst_t(n_traces, 0.0);
+  std::vector<int> err_t(n_traces, 0);
+  std::vector<Invalid> err_v(n_traces);
+  auto one = [&](int t, std::vector<uint32_t>& last) {
     const cace_trace_t& tr = traces[t];
     const int64_t n = tr.n_requests, b = L.off[t];
     if (n > 0 && (!tr.arrival_time_s || !tr.model || !tr.prompt_tokens || !tr.output_tokens))
@@ -131,29 +168,61 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
         return tr.arrival_time_s[x] < tr.arrival_time_s[y];
       });
     for (int m = 0; m < M; ++m) last[m] = (uint32_t)n;
+    double worst = 0.0;
+    uint32_t ncomp = 0;
+    int bad = -1;
     for (int64_t k = n - 1; k >= 0; --k) {
       const uint32_t i = ord[k];
       const int m = tr.model[i];
-      ReqRec& r = L.rec[b + k];
+      ReqRec& r = rec[b + k];
       r.arrival = tr.arrival_time_s[i];
       // service_times (engine.cpp:15-26)
       r.prefill = (double)tr.prompt_tokens[i] / cat.pr[m];
       r.decode = (double)std::max(tr.output_tokens[i], 1) / cat.dr[m];
       r.nxt = last[m];
-      r.nxa = last[m] < (uint32_t)n ? L.rec[b + last[m]].arrival : INFINITY;
+      r.nxa = last[m] < (uint32_t)n ? rec[b + last[m]].arrival : INFINITY;
       r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
+      r.pad = 0.0;
+      worst = std::max(worst, r.prefill + r.decode);
       last[m] = (uint32_t)k;
       L.perm[b + k] = i;
-      L.ncomp[t] += cat.cls[m] == CACE_REASONING ? 0u : 1u;
-      if (cat.bad_rates(m)) L.bad_model[t] = m;  // ends as the first in replay order
+      ncomp += cat.cls[m] == CACE_REASONING ? 0u : 1u;
+      if (cat.bad_rates(m)) bad = m;  // ends as the first in replay order
     }
+    // per-trace results written once (no false sharing between threads)
+    worst_t[t] = worst;
+    L.ncomp[t] = ncomp;
+    L.bad_model[t] = bad;
     for (int m = 0; m < M; ++m) L.first0[(size_t)t * M + m] = last[m];
+  };
+  const int nth = (int)std::min<int64_t>(
+      {(int64_t)std::max(1u, std::thread::hardware_concurrency()), (int64_t)n_traces, (int64_t)32,
+       std::max<int64_t>(1, N / 65536)});
+  auto worker = [&](int w) {
+    std::vector<uint32_t> last(M);
+    for (int t = w; t < n_traces; t += nth) {
+      try {
+        one(t, last);
+      } catch (const Invalid& x) {
+        err_t[t] = 1;
+        err_v[t] = x;
+      }
+    }
+  };
+  if (nth <= 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nth; ++w) pool.emplace_back(worker, w);
+    for (auto& th : pool) th.join();
   }
+  for (int t = 0; t < n_traces; ++t)
+    if (err_t[t]) throw err_v[t];
   // Event times stay < 1e30 (the kernels' fp32 screening relies on it): the
   // clock advances by at most one load (+ unload) and one service per request.
   double worst = 0.0;
   for (int m = 0; m < M; ++m) worst = std::max(worst, cat.lt[m]);
-  for (const ReqRec& r : L.rec) worst = std::max(worst, r.prefill + r.decode);
+  for (int t = 0; t < n_traces; ++t) worst = std::max(worst, worst_t[t]);
   if (!(worst * (double)(N + 1) < 1e28))
     throw Invalid{CACE_E_INVALID, "cace: load/service times too large (event clock would exceed 1e28 s)"};
 }

@@ -18,7 +18,7 @@ def build():
         return SO
     os.makedirs(os.path.dirname(SO), exist_ok=True)
     cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
-    subprocess.run([cxx, "-std=c++17", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-o", SO, SRCS[0]],
+    subprocess.run([cxx, "-std=c++17", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-pthread", "-o", SO, SRCS[0]],
                    check=True)
     return SO
 
