@@ -301,8 +301,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const bool need_win = !is_lru && variant != CACE_MINUS_P3;
   const bool verbatim = sc.p1_mode == CACE_P1_VERBATIM;
   const uint32_t w = (uint32_t)sc.window_length;
-  const double wd = (double)sc.window_length;
-  const double unload = sc.unload_time_s;
   const double norm = (double)sc.output_token_normalizer;
   const float rcpw = 1.0f / (float)sc.window_length;
   // fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0
@@ -351,13 +349,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     stime[s] = 0.0;
   }
   int occ = 0;
-  uint32_t seqc = 0;
   Cursor cur{-INFINITY, 2, 0};
 
   // loads == misses == n - hits; evictions == loads - final occupancy.
   uint32_t hits = 0;
-  double lo_sum = 0.0, sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
-  uint64_t ho = CACE_HASH_SEED, he = CACE_HASH_SEED;
+  double sttft = 0.0, se2e = 0.0, mttft = 0.0, me2e = 0.0;
+  uint64_t ho = CACE_HASH_SEED;
+  double lo_sum = 0.0;
+  uint64_t he = CACE_HASH_SEED;
+  const double unload = sc.unload_time_s;
 
   for (uint32_t c = 0, k = 0; k < n; ++c) {
   const ReqRec* const cb = rs.chunk(c);
@@ -400,16 +400,18 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         // times break ties on the push seq.
         cur = Cursor{td, 1, tq};
         const double ntd = -td;
-        bool tie = false;
+        int neq = 0;  // slots completing exactly at td, hs included
 #pragma unroll
         for (int s = 0; s < C; ++s) {
           if (stime[s] > ntd) stime[s] = fabs(stime[s]);
-          tie |= s != hs && stime[s] == ntd;
+          neq += stime[s] == ntd ? 1 : 0;
         }
-        if (tie) {
+        if (neq > 1) {
+          // equal completion times pop in push order: earlier seq -> Idle
+          // (hs itself has seq == tq and is overwritten by the service below)
 #pragma unroll
           for (int s = 0; s < C; ++s)
-            if (s != hs && stime[s] == ntd && S.seq[s * st] <= tq) stime[s] = td;
+            if (stime[s] == ntd && S.seq[s * st] < tq) stime[s] = fabs(stime[s]);
         }
       }
     } else {
@@ -514,7 +516,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 double p3 = 0.0;
                 if (variant != CACE_MINUS_P3) {
                   const WinEnt e = win.gather(ms);
-                  p3 = (e.f - k < w && e.fa < now) ? (double)e.r / wd : 1.0;
+                  p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
                 }
                 const double p4 = S.p4d[ms * st];
                 const double T = ((p1 + p2) + p3) + p4;
@@ -576,8 +578,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     for (int s = 0; s < C; ++s)
       if (s == hs) stime[s] = -done;
     S.done[hs * st] = done;
-    S.seq[hs * st] = seqc;
-    ++seqc;
+    S.seq[hs * st] = k;  // push seq: services start once per request, in order
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
       mttft = ttft > mttft ? ttft : mttft;
@@ -684,7 +685,8 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   const bool warp_win = __any_sync(kFull, need_win);
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x,
-                   l_seq + threadIdx.x,  l_slot + threadIdx.x, LANE_BLOCK, w_rec, w_win};
+                   l_seq + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
+                   w_rec, w_win};
   replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);
 }
 #endif  // CACE_HOST_EMULATION
