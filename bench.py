@@ -154,7 +154,9 @@ def run_reference_arm(args):
         return
     catalog, traces, sc = workload(args)
     threads = os.cpu_count() or 1
-    per_step = max(2 * threads, 8) if args.config == 4 else max(threads // 4, 2)
+    # enough scenarios per step to keep every host thread busy (cost varies
+    # with the window length), bounded so the whole run takes ~a minute
+    per_step = max(4 * threads, 16) if args.config == 4 else max(threads // 4, 2)
     rng = np.random.default_rng(777)
     times, reqs = [], []
     kind = "reference"
@@ -304,7 +306,13 @@ def main():
         if world > 1:
             tl = all_reduce(tl, torch.distributed.ReduceOp.MAX)
         n_all = sum(len(t) for t in traces)
-        h2d = n_all * (8 + 4 + 4 + 4) + len(sc) * sc.dtype.itemsize
+        # bytes cace_replay_batch copies: 48-B replay records + 4-B permutation
+        # per request, per-trace offsets / first occurrences, the scenarios,
+        # the plan order (8 B per scenario + warp padding, bounded by 32 per
+        # (capacity, trace) group) and the catalog / log tables
+        n_groups = len(np.unique(sc[["num_accelerators", "models_per_accelerator", "trace"]]))
+        h2d = (n_all * (48 + 4) + len(traces) * (8 + 4 * len(catalog) + 4) + len(sc) * (sc.dtype.itemsize + 8)
+               + n_groups * 31 * 8 + len(catalog) * 36 + 2 * 256 * 8)
         d2h = len(sc) * SUMMARY_DTYPE.itemsize
         e2e = {"value": S_total * n_req / (float(tl.item()) / 1e3), "unit": "scenario-requests/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -319,6 +327,15 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved_gbs = (len(sc) * n_req * B_ALG) / (t_local / 1e3) / 1e9
+    # measured DRAM traffic of the same step (ncu launch list, committed)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        key = f"cfg{args.config}_n{n_req}_s{S_total}"
+        if key in tr and world == 1:
+            traffic = tr[key]["dram_bytes_per_step"]
+    except Exception:
+        pass
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -350,10 +367,12 @@ def main():
                    "vectors_stride": args.vectors_stride},
         "eviction_decisions_per_s": evictions / (t_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": None,
-                     "kernel": "replay_lane_kernel<C> (all capacity instantiations of one step)",
-                     "note": "achieved = 18 B algorithmic per scenario-request / step time; physical DRAM traffic "
-                             "is far lower (traces are L2-resident and shared by every lane), see profiles/"},
+                     "frac": achieved_gbs / hbm, "traffic": traffic,
+                     "kernel": "replay_lane_kernel<C> (the step = one launch per capacity, run concurrently)",
+                     "note": "achieved = 18 B algorithmic per scenario-request x scenario-requests of the step / "
+                             "step time (CUDA events on the launch stream); traffic = ncu dram read+write bytes of "
+                             "the step's launches (profiles/traffic.json): the trace is L2-resident and shared by "
+                             "every lane, so the kernel is issue-bound, not HBM-bound (profiles/)"},
         "gpu_launches": launches,
         "status_ok": status_ok,
         "clocks": clk.summary(),

@@ -17,6 +17,6 @@ timeout 600 python bench.py --impl reference > $OUT/bench_ref_$TAG.log 2>&1
 echo "rc=$?" >> $OUT/bench_ref_$TAG.log
 timeout 900 python bench.py --config 5 --requests ${CFG5_N:-1000000} --scenarios ${CFG5_S:-2048} --steps 2 --warmup 1 --e2e-steps 1 --cpu-sample 4 > $OUT/bench_cfg5_$TAG.log 2>&1
 echo "rc=$?" >> $OUT/bench_cfg5_$TAG.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_$TAG.log 2>&1
 echo "rc=$?" >> $OUT/ncu_launch_$TAG.log
