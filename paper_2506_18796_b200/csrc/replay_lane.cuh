@@ -280,6 +280,7 @@ struct LaneSmem {
   double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67)
   double* done;      // [C] |stime|: completion time of the slot's last service
   uint32_t* seq;     // [C] ServiceComplete push seq of each busy slot
+  int* word;         // [C] slot word: model | lex rank << 18
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
   int stride;
   ReqRec* rec;       // warp: record double buffer [64]
@@ -341,11 +342,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 
   // Slots (registers), sign-encoded (file comment); the push seq (tie-break
   // of equal completion times) lives in shared memory.
-  int sms[C];
   double stime[C];
 #pragma unroll
   for (int s = 0; s < C; ++s) {
-    sms[s] = 0xffff;
+    S.word[s * st] = 0xffff;
     stime[s] = 0.0;
   }
   int occ = 0;
@@ -449,7 +449,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             int flex = 0;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              const int lx = slot_lex(sms[s]);
+              const int lx = slot_lex(S.word[s * st]);
               if (is_idle(stime[s]) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
                 f = s;
                 flu = stime[s];
@@ -476,7 +476,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              const int ms = slot_model(sms[s]);
+              const int ms = slot_model(S.word[s * st]);
               const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
               const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
               const float p1 = fmaf(p1s, p1v, p1o);
@@ -507,8 +507,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 #pragma unroll
               for (int s = 0; s < C; ++s) {
                 if (!is_idle(stime[s])) continue;
-                const int ms = slot_model(sms[s]);
-                const int lx = slot_lex(sms[s]);
+                const int wd = S.word[s * st];
+                const int ms = slot_model(wd);
+                const int lx = slot_lex(wd);
                 const double p1 = variant == CACE_MINUS_P1
                                       ? 0.0
                                       : exact_p1(now, stime[s], verbatim, P.log_variant, P.log_tab, P.log_tab2);
@@ -534,10 +535,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           }
         }
         // residents.erase(victim); evictions++ (engine.cpp:205-206)
-        int vm = 0;
-#pragma unroll
-        for (int s = 0; s < C; ++s)
-          if (s == v) vm = slot_model(sms[s]);
+        const int vm = slot_model(S.word[v * st]);
         S.slot_of[vm * st] = 0;
         he = hmix(he, dbits(cur.t) ^ ((uint64_t)vm << 32));
         if (DUMP && dslot >= 0) {
@@ -556,9 +554,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       lw = r - cur.t;
       lo_sum += lt;
       const int word = m | (K.lex[m] << 18);
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (s == v) sms[s] = word;
+      S.word[v * st] = word;
       S.slot_of[m * st] = (uint8_t)(v + 1);
       const double nr = -r;
 #pragma unroll
@@ -637,7 +633,7 @@ constexpr int LANE_BLOCK = 128;
 // window table.
 inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
 inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
-  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + C * 4 + M);
+  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + C * 8 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M) { return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt); }
 inline size_t lane_smem_bytes(int M, int C) {
@@ -660,7 +656,8 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   double* l_done = l_p4d + (size_t)M * LANE_BLOCK;                                          // [C][LB]
   float* l_p4f = reinterpret_cast<float*>(l_done + (size_t)C * LANE_BLOCK);                // [M][LB]
   uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_p4f + (size_t)M * LANE_BLOCK);  // [C][LANE_BLOCK]
-  uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_seq + (size_t)C * LANE_BLOCK);   // [M][LANE_BLOCK]
+  int* l_word = reinterpret_cast<int*>(l_seq + (size_t)C * LANE_BLOCK);          // [C][LANE_BLOCK]
+  uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_word + (size_t)C * LANE_BLOCK);  // [M][LANE_BLOCK]
   unsigned char* wbase =
       smem + ((((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
       (size_t)(threadIdx.x >> 5) * lane_smem_warp(M);
@@ -685,7 +682,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_
   const bool warp_win = __any_sync(kFull, need_win);
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x,
-                   l_seq + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
+                   l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win};
   replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);
 }

@@ -49,8 +49,9 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   std::vector<float> p4f(P.cat.M);
   std::vector<double> p4d(P.cat.M), done(C);
   std::vector<uint32_t> seq(C);
+  std::vector<int> word(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), p4d.data(), done.data(), seq.data(), slot_of.data(), 1, nullptr, nullptr};
+  const LaneSmem S{p4f.data(), p4d.data(), done.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr};
   replay_scenario<C, 2, D>(P, i, false, need_win, K, S);
 }
 
