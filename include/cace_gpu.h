@@ -16,6 +16,8 @@
  *   cace_dedup_window_batch  <- LookaheadWindow dedup_window(...)           policy.hpp:56-57
  *   cace_service_times_batch <- std::pair<double,double> service_times(...) engine.hpp:54-55
  *   cace_log_selftest        <- the libm log the reference calls             policy.cpp:51
+ *   cace_run_metrics_batch   <- RunMetrics compute_run_metrics(const SimulationReport&)
+ *                               for every replay of a sweep                 metrics.hpp:29-31
  *
  * Error behaviour: every entry returns CACE_OK (0) or one CACE_E_* code per
  * SimError site of the reference, and writes the reference's message text
@@ -51,6 +53,9 @@ enum {
   CACE_E_DEADLOCK = 6,      /* "run: deadlock — pending requests ..."       engine.cpp:235-237 */
   CACE_E_RESIDENCY = 7,     /* "run: residency bound violated"              engine.cpp:118-120 */
   CACE_E_DEDUP_LENGTH = 8,  /* "dedup_window: length must be >= 1"          policy.cpp:23 */
+  CACE_E_METRICS_EMPTY = 9, /* "compute_run_metrics: empty report"           metrics.cpp:37-39 */
+  CACE_E_METRICS_NO_TTFT = 10, /* "...: no completion outcomes for TTFT"     metrics.cpp:53-55 */
+  CACE_E_METRICS_NO_E2E = 11,  /* "...: no reasoning outcomes for E2E"       metrics.cpp:56-58 */
   CACE_E_INVALID = 20,      /* malformed call (null pointer, bad index, unsupported size) */
   CACE_E_CUDA = 21,         /* CUDA runtime error (message has the CUDA text) */
   CACE_E_NO_DEVICE = 22     /* no CUDA device: there is no CPU fallback */
@@ -134,6 +139,21 @@ typedef struct {
 #define CACE_HASH_MUL_LO 0x9e3779b1u
 #define CACE_HASH_MUL_HI 0x85ebca77u
 
+/* LatencySummary (metrics.hpp:11-18) and RunMetrics (metrics.hpp:23-29). */
+typedef struct {
+  uint64_t count;
+  double mean_s, p50_s, p95_s, p99_s, max_s;
+} cace_latency_summary_t;
+typedef struct {
+  double cache_hit_rate;
+  double load_overhead_s;
+  double evictions;
+  cace_latency_summary_t ttft_completion;
+  cace_latency_summary_t e2e_reasoning;
+  int32_t status; /* CACE_OK, the replay's status, or CACE_E_METRICS_* */
+  int32_t reserved;
+} cace_run_metrics_t;
+
 /* Optional full dump for a few scenarios: per-request RequestOutcome fields
  * (engine.hpp:19-30) indexed by the caller's request index, and the
  * eviction log (victim model, clock) in eviction order.  Any pointer may be
@@ -181,6 +201,22 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
                           int32_t n_traces, const cace_scenario_t* scenarios, int64_t n_scenarios,
                           cace_summary_t* summaries, const cace_dump_t* dump,
                           const cace_opts_t* opts, char* msg, size_t msg_cap);
+
+/* compute_run_metrics (metrics.cpp:35-62) of every scenario's replay,
+ * computed on the device: the replay captures each scenario's TTFT /
+ * E2E samples, one CTA per (scenario, task class) selects the nearest-rank
+ * p50 / p95 / p99 and max exactly (metrics.cpp:14-33), and the counters come
+ * from the replay summary.  count, percentiles, max, hit rate, load overhead
+ * and evictions are bit-identical to the reference; mean_s divides the
+ * replay-order sum (the reference sums the sorted samples, metrics.cpp:26), so
+ * it agrees to ~1e-15 relative.  Scenarios are processed in batches sized to
+ * the free device memory.  summaries (optional, NULL) receives the replay
+ * summaries too.  Host memory. */
+int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                               int32_t n_traces, const cace_scenario_t* scenarios,
+                               int64_t n_scenarios, cace_run_metrics_t* metrics,
+                               cace_summary_t* summaries, const cace_opts_t* opts, char* msg,
+                               size_t msg_cap);
 
 /* Device-resident engine for repeated sweeps (bench, multi-GPU shards):
  * the catalog and traces are uploaded and pre-laid-out once; replays then

@@ -98,6 +98,8 @@ def lib():
         L.ref_run.restype = i32
         L.ref_run.argtypes = [vp, vp, vp, vp, vp, i64, P(RefScenario), P(RefCounters),
                               vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64), cp, sz]
+        L.ref_run_metrics.restype = i32
+        L.ref_run_metrics.argtypes = [vp, vp, vp, vp, vp, i64, P(RefScenario), vp, vp, C.c_char_p, C.c_size_t]
         L.ref_dedup_window.restype = i32
         L.ref_dedup_window.argtypes = [vp, vp, i32, i32, vp, P(i32), cp, sz]
         L.ref_eviction_score.restype = i32
@@ -226,6 +228,25 @@ def run(cat: Catalog, trace: dict, sc: RefScenario) -> RefReport:
     return RefReport(cnt.hits, cnt.misses, cnt.evictions, cnt.loads, cnt.load_overhead_s,
                      cnt.max_resident, cold.astype(bool), f["qw"], f["lw"], f["pf"], f["dc"],
                      f["ttft"], f["e2e"], ev_m[:k].copy(), ev_c[:k].copy())
+
+
+def run_metrics(cat: Catalog, trace: dict, sc: RefScenario) -> dict:
+    """Reference ``compute_run_metrics(run(...))`` (metrics.cpp:35-62)."""
+    arr = np.ascontiguousarray(trace["arrival"], np.float64)
+    mdl = np.ascontiguousarray(trace["model"], np.int32)
+    pr = np.ascontiguousarray(trace["prompt"], np.int32)
+    out = np.ascontiguousarray(trace["output"], np.int32)
+    vals = np.zeros(13, np.float64)
+    cnt = np.zeros(2, np.uint64)
+    msg = C.create_string_buffer(1024)
+    rc = lib().ref_run_metrics(cat._h, _ptr(arr), _ptr(mdl), _ptr(pr), _ptr(out), len(arr), C.byref(sc),
+                               _ptr(vals), _ptr(cnt), msg, 1024)
+    _check(rc, msg)
+    res = {"cache_hit_rate": vals[0], "load_overhead_s": vals[1], "evictions": vals[2]}
+    for c, name in enumerate(("ttft_completion", "e2e_reasoning")):
+        res[name] = {"count": int(cnt[c]), **{q: vals[3 + 5 * c + j]
+                                              for j, q in enumerate(("mean_s", "p50_s", "p95_s", "p99_s", "max_s"))}}
+    return res
 
 
 def dedup_window(cat: Catalog, pending, length: int):

@@ -35,6 +35,7 @@
 
 #include "cacesim/catalog.hpp"
 #include "cacesim/engine.hpp"
+#include "cacesim/metrics.hpp"
 #include "cacesim/policy.hpp"
 #include "cacesim/types.hpp"
 #include "cacesim/workload.hpp"
@@ -346,6 +347,41 @@ int32_t ref_run(void* catp, const double* arrival, const int32_t* model_idx, con
     return 1;
   } catch (const std::exception& e) {
     g_rec.active = false;
+    put_msg(msg, mcap, e.what());
+    return 2;
+  }
+}
+
+// Reference compute_run_metrics (metrics.cpp:35-62) of one run():
+// out = {hit_rate, load_overhead_s, evictions, ttft{mean,p50,p95,p99,max},
+// e2e{mean,p50,p95,p99,max}}, counts = {ttft count, e2e count}.
+int32_t ref_run_metrics(void* catp, const double* arrival, const int32_t* model_idx,
+                        const int32_t* prompt, const int32_t* output, int64_t n,
+                        const ref_scenario_t* sc, double* out, uint64_t* counts, char* msg,
+                        size_t mcap) {
+  try {
+    const ModelCatalog& cat = *static_cast<ModelCatalog*>(catp);
+    Trace t = make_trace(cat, arrival, model_idx, prompt, output, n);
+    Policy pol = make_policy(to_policy(*sc));
+    SimulationReport rep = run(t, cat, to_cluster(*sc), pol);
+    RunMetrics m = compute_run_metrics(rep);
+    out[0] = m.cache_hit_rate;
+    out[1] = m.load_overhead_s;
+    out[2] = m.evictions;
+    const LatencySummary* ls[2] = {&m.ttft_completion, &m.e2e_reasoning};
+    for (int c = 0; c < 2; ++c) {
+      counts[c] = ls[c]->count;
+      out[3 + 5 * c + 0] = ls[c]->mean_s;
+      out[3 + 5 * c + 1] = ls[c]->p50_s;
+      out[3 + 5 * c + 2] = ls[c]->p95_s;
+      out[3 + 5 * c + 3] = ls[c]->p99_s;
+      out[3 + 5 * c + 4] = ls[c]->max_s;
+    }
+    return 0;
+  } catch (const SimError& e) {
+    put_msg(msg, mcap, e.what());
+    return 1;
+  } catch (const std::exception& e) {
     put_msg(msg, mcap, e.what());
     return 2;
   }

@@ -22,14 +22,16 @@ from .api import (  # noqa: F401
     TaskClass,
     Trace,
     Variant,
+    average_metrics,
     dedup_window,
     device_count,
     eviction_score,
     make_scenarios,
     run,
     run_batch,
+    run_metrics,
     select_victim,
     service_times,
     version,
 )
-from ._native import SCENARIO_DTYPE, SUMMARY_DTYPE  # noqa: F401
+from ._native import METRICS_DTYPE, SCENARIO_DTYPE, SUMMARY_DTYPE  # noqa: F401

@@ -25,6 +25,9 @@ CACE_E_CLOCK = 5
 CACE_E_DEADLOCK = 6
 CACE_E_RESIDENCY = 7
 CACE_E_DEDUP_LENGTH = 8
+CACE_E_METRICS_EMPTY = 9
+CACE_E_METRICS_NO_TTFT = 10
+CACE_E_METRICS_NO_E2E = 11
 CACE_E_INVALID = 20
 CACE_E_CUDA = 21
 CACE_E_NO_DEVICE = 22
@@ -77,6 +80,18 @@ SUMMARY_DTYPE = np.dtype(
 )
 assert SUMMARY_DTYPE.itemsize == 112
 
+# LatencySummary / RunMetrics (metrics.hpp:11-29) as cace_run_metrics_t.
+LATENCY_DTYPE = np.dtype([("count", "<u8"), ("mean_s", "<f8"), ("p50_s", "<f8"), ("p95_s", "<f8"),
+                          ("p99_s", "<f8"), ("max_s", "<f8")])
+METRICS_DTYPE = np.dtype(
+    [
+        ("cache_hit_rate", "<f8"), ("load_overhead_s", "<f8"), ("evictions", "<f8"),
+        ("ttft_completion", LATENCY_DTYPE), ("e2e_reasoning", LATENCY_DTYPE),
+        ("status", "<i4"), ("reserved", "<i4"),
+    ]
+)
+assert METRICS_DTYPE.itemsize == 128
+
 
 class DumpABI(C.Structure):
     _fields_ = [
@@ -111,7 +126,7 @@ EXPORTED = [
     "cace_engine_create", "cace_engine_destroy", "cace_engine_plan", "cace_engine_replay_device",
     "cace_engine_status_message", "cace_engine_last_launches", "cace_select_victim_batch",
     "cace_eviction_score_batch", "cace_dedup_window_batch", "cace_service_times_batch",
-    "cace_log_selftest", "cace_log_host", "cace_probe_log_variant",
+    "cace_log_selftest", "cace_log_host", "cace_probe_log_variant", "cace_run_metrics_batch",
 ]
 
 
@@ -130,6 +145,8 @@ def _load():
     L.cace_device_count.restype = i32
     L.cace_replay_batch.restype = i32
     L.cace_replay_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, P(DumpABI), P(OptsABI), C.c_char_p, sz]
+    L.cace_run_metrics_batch.restype = i32
+    L.cace_run_metrics_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, vp, P(OptsABI), C.c_char_p, sz]
     L.cace_engine_create.restype = i32
     L.cace_engine_create.argtypes = [P(CatalogABI), vp, i32, P(OptsABI), P(vp), C.c_char_p, sz]
     L.cace_engine_destroy.argtypes = [vp]

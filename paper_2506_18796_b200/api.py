@@ -384,6 +384,53 @@ def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray,
     return summ, reports
 
 
+def run_metrics(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray, device: int = 0,
+                raise_on_error: bool = True, kernel: int = KERNEL_AUTO, with_summaries: bool = False):
+    """``compute_run_metrics`` (metrics.cpp:35-62) of every scenario's replay,
+    computed on the GPU (``cace_run_metrics_batch``): a METRICS_DTYPE array
+    (cache hit rate, load overhead, evictions, nearest-rank TTFT/E2E
+    summaries).  Scenarios whose metrics the reference could not compute
+    carry a non-zero ``status`` (raised as SimError when ``raise_on_error``)."""
+    scenarios = np.ascontiguousarray(scenarios, SCENARIO_DTYPE)
+    out = np.zeros(len(scenarios), N.METRICS_DTYPE)
+    summ = np.zeros(len(scenarios), SUMMARY_DTYPE) if with_summaries else None
+    tarr = _trace_array(traces)
+    msg = C.create_string_buffer(1024)
+    opts = _opts(device, kernel=kernel)
+    rc = N.lib.cace_run_metrics_batch(C.byref(catalog.abi()), C.cast(tarr, C.c_void_p), len(traces),
+                                      ptr(scenarios), len(scenarios), ptr(out), ptr(summ), C.byref(opts), msg,
+                                      1024)
+    if rc != N.CACE_OK and (raise_on_error or rc >= N.CACE_E_INVALID):
+        _raise(rc, msg)
+    return (out, summ) if with_summaries else out
+
+
+def average_metrics(runs: np.ndarray) -> np.ndarray:
+    """``average_metrics`` (metrics.cpp:89-104): elementwise mean over the
+    per-seed RunMetrics of one grid cell, summed in the given order."""
+    runs = np.asarray(runs, N.METRICS_DTYPE)
+    if len(runs) == 0:
+        raise SimError("average_metrics: no runs")
+    k = float(len(runs))
+    avg = np.zeros((), N.METRICS_DTYPE)
+    for f in ("cache_hit_rate", "load_overhead_s", "evictions"):
+        acc = 0.0
+        for r in runs:
+            acc += float(r[f])
+        avg[f] = acc / k
+    for lf in ("ttft_completion", "e2e_reasoning"):
+        cnt = 0
+        sums = {q: 0.0 for q in ("mean_s", "p50_s", "p95_s", "p99_s", "max_s")}
+        for r in runs:
+            cnt += int(r[lf]["count"])
+            for q in sums:
+                sums[q] += float(r[lf][q])
+        avg[lf]["count"] = cnt
+        for q, v in sums.items():
+            avg[lf][q] = v / k
+    return avg
+
+
 def run(trace: Trace, catalog: ModelCatalog, cluster: ClusterConfig = ClusterConfig(),
         policy: PolicyConfig = PolicyConfig(), device: int = 0, kernel: int = KERNEL_AUTO) -> SimulationReport:
     """``cacesim::run`` (engine.cpp:76-239) on the GPU: one scenario, full report."""

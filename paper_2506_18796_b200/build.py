@@ -1,6 +1,8 @@
 """In-tree build of the CUDA engine (``lib/libcace_gpu.so``) for sm_100a.
 
-``python -m paper_2506_18796_b200.build`` (or ``__graft_entry__.build()``).
+``python paper_2506_18796_b200/build.py`` (or ``__graft_entry__.build()``); running it
+as a script does not import the package, which refuses to load without the
+library.
 nvcc cross-compiles here without a GPU; the .so travels with the repo
 snapshot to the GPU box.
 

@@ -20,6 +20,7 @@
 #include "replay_lane.cuh"
 #include "replay_warp.cuh"
 #include "layout.hpp"
+#include "metrics.cuh"
 
 using namespace cace;
 
@@ -732,6 +733,121 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
   });
   cace_engine_destroy(e);
   pt.mark("destroy");
+  return rc;
+}
+
+
+int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                               int32_t n_traces, const cace_scenario_t* scenarios,
+                               int64_t n_scenarios, cace_run_metrics_t* metrics,
+                               cace_summary_t* summaries, const cace_opts_t* opts, char* msg,
+                               size_t msg_cap) {
+  cace_engine* e = nullptr;
+  int32_t rc = cace_engine_create(catalog, traces, n_traces, opts, &e, msg, msg_cap);
+  if (rc != CACE_OK) return rc;
+  rc = guarded(msg, msg_cap, [&]() -> int32_t {
+    if (n_scenarios > 0 && (!metrics || !scenarios))
+      throw Invalid{CACE_E_INVALID, "cace: metrics / scenarios is NULL"};
+    cudaStream_t s = e->stream;
+    std::vector<cace_summary_t> summ(n_scenarios);
+    // sample budget per batch: ~60% of free device memory
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = std::max<size_t>((size_t)(0.6 * (double)free_b), (size_t)64 << 20);
+    auto nreq = [&](int64_t i) -> int64_t {
+      const int t = scenarios[i].trace;
+      return (t >= 0 && t < e->lay.T) ? e->lay.off[t + 1] - e->lay.off[t] : 0;
+    };
+    std::vector<double> stat;
+    for (int64_t b0 = 0; b0 < n_scenarios;) {
+      int64_t b1 = b0;
+      size_t bytes = 0;
+      while (b1 < n_scenarios && (b1 == b0 || bytes + (size_t)nreq(b1) * 8 <= budget)) bytes += (size_t)nreq(b1++) * 8;
+      const int64_t B = b1 - b0;
+      const cace_scenario_t* sc = scenarios + b0;
+      plan(e, sc, B);
+      std::vector<int32_t> slot(B);
+      std::vector<int64_t> off(B + 1, 0);
+      std::vector<uint32_t> nc(B), nr(B);
+      for (int64_t i = 0; i < B; ++i) {
+        slot[i] = (int32_t)i;
+        const int t = sc[i].trace;
+        const bool tv = t >= 0 && t < e->lay.T;
+        nr[i] = (uint32_t)nreq(b0 + i);
+        nc[i] = tv ? e->lay.ncomp[t] : 0;
+        off[i + 1] = off[i] + nr[i];
+      }
+      DBuf<cace_scenario_t> d_sc;
+      d_sc.upload(sc, B, s);
+      DBuf<cace_summary_t> d_out;
+      d_out.alloc(B, s);
+      DBuf<int32_t> d_slot;
+      DBuf<int64_t> d_off;
+      DBuf<uint32_t> d_nc, d_nr;
+      DBuf<double> d_samp, d_stat;
+      d_slot.upload(slot.data(), B, s);
+      d_off.upload(off.data(), B + 1, s);
+      d_nc.upload(nc.data(), B, s);
+      d_nr.upload(nr.data(), B, s);
+      d_samp.alloc(std::max<int64_t>(off[B], 1), s);
+      d_stat.alloc((size_t)B * 8, s);
+      DumpDev dd{};
+      dd.slot = d_slot.p;
+      dd.dump_off = d_off.p;
+      dd.samples = d_samp.p;
+      replay(e, d_sc.p, B, d_out.p, dd, s);
+      MetricsParams mp{d_samp.p, d_off.p, d_nc.p, d_nr.p, d_stat.p};
+      if (B > 0) metrics_select_kernel<<<(unsigned)(2 * B), METRICS_BLOCK, 0, s>>>(mp);
+      CK(cudaGetLastError());
+      stat.resize((size_t)B * 8);
+      CK(cudaMemcpyAsync(summ.data() + b0, d_out.p, B * sizeof(cace_summary_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(stat.data(), d_stat.p, (size_t)B * 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      // RunMetrics (compute_run_metrics, metrics.cpp:35-62)
+      for (int64_t i = 0; i < B; ++i) {
+        const cace_summary_t& o = summ[b0 + i];
+        cace_run_metrics_t& m = metrics[b0 + i];
+        std::memset(&m, 0, sizeof(m));
+        m.status = o.status;
+        if (o.status != CACE_OK) continue;
+        if (o.hits + o.misses == 0) {
+          m.status = CACE_E_METRICS_EMPTY;
+          continue;
+        }
+        if (nc[i] == 0) {
+          m.status = CACE_E_METRICS_NO_TTFT;
+          continue;
+        }
+        if (nr[i] - nc[i] == 0) {
+          m.status = CACE_E_METRICS_NO_E2E;
+          continue;
+        }
+        m.cache_hit_rate = (double)o.hits / (double)(o.hits + o.misses);
+        m.load_overhead_s = o.load_overhead_s;
+        m.evictions = (double)o.evictions;
+        const double* st = stat.data() + (size_t)i * 8;
+        auto fill = [&](cace_latency_summary_t& ls, uint64_t cnt, double sum, const double* q) {
+          ls.count = cnt;
+          ls.mean_s = sum / (double)cnt;  // replay-order sum (the reference sums the sorted samples)
+          ls.p50_s = q[0];
+          ls.p95_s = q[1];
+          ls.p99_s = q[2];
+          ls.max_s = q[3];
+        };
+        fill(m.ttft_completion, nc[i], o.sum_ttft_completion, st);
+        fill(m.e2e_reasoning, nr[i] - nc[i], o.sum_e2e_reasoning, st + 4);
+      }
+      b0 = b1;
+    }
+    if (summaries && n_scenarios > 0) std::memcpy(summaries, summ.data(), n_scenarios * sizeof(cace_summary_t));
+    for (int64_t i = 0; i < n_scenarios; ++i)
+      if (metrics[i].status != CACE_OK) {
+        put_msg(msg, msg_cap, status_text(e->cat, metrics[i].status));
+        return metrics[i].status & 0xff;
+      }
+    return CACE_OK;
+  });
+  cace_engine_destroy(e);
   return rc;
 }
 

@@ -182,12 +182,21 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
       r.nxt = last[m];
       r.nxa = last[m] < (uint32_t)n ? rec[b + last[m]].arrival : INFINITY;
       r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
-      r.pad = 0.0;
+      // same-class requests after k (turned into the class-local index below)
+      r.ci = cat.cls[m] == CACE_REASONING ? (uint32_t)(n - 1 - k) - ncomp : ncomp;
+      r.pad = 0;
       worst = std::max(worst, r.prefill + r.decode);
       last[m] = (uint32_t)k;
       L.perm[b + k] = i;
       ncomp += cat.cls[m] == CACE_REASONING ? 0u : 1u;
       if (cat.bad_rates(m)) bad = m;  // ends as the first in replay order
+    }
+    // class-local index (position among the same-class requests)
+    const uint32_t nreas = (uint32_t)n - ncomp;
+    for (int64_t k = 0; k < n; ++k) {
+      ReqRec& r = rec[b + k];
+      const bool reas = (r.mc >> 16) != 0;
+      r.ci = (reas ? nreas : ncomp) - 1 - r.ci;
     }
     // per-trace results written once (no false sharing between threads)
     worst_t[t] = worst;
@@ -261,6 +270,9 @@ inline std::string status_text(const HostCatalog& cat, int32_t status) {
     case CACE_E_DEADLOCK:
       return "run: deadlock \xe2\x80\x94 pending requests with no schedulable event";
     case CACE_E_RESIDENCY: return "run: residency bound violated";
+    case CACE_E_METRICS_EMPTY: return "compute_run_metrics: empty report";
+    case CACE_E_METRICS_NO_TTFT: return "compute_run_metrics: no completion outcomes for TTFT";
+    case CACE_E_METRICS_NO_E2E: return "compute_run_metrics: no reasoning outcomes for E2E";
     default:
       if (code == CACE_E_INVALID && m == 1) return "cace: unload_time_s must be in [0, 1e15)";
       if (code == CACE_E_INVALID && m == 2) return "cace: capacity > 64 is not supported";

@@ -1,0 +1,145 @@
+// Per-scenario order statistics for RunMetrics (compute_run_metrics,
+// metrics.cpp:35-62; nearest-rank summarize, metrics.cpp:14-33).
+//
+// The replay kernels (DUMP instantiation with dump.samples set) write, per
+// scenario, the TTFT of its completion requests followed by the E2E of its
+// reasoning requests.  One CTA per (scenario, class) segment then finds the
+// nearest-rank p50 / p95 / p99 and the max by an MSD radix select over the
+// samples' IEEE bit patterns (latencies are >= +0, so unsigned order is
+// numeric order): 8 passes of 8 bits, one 256-bin shared histogram per
+// distinct target prefix, warp-aggregated increments (__match_any_sync) so
+// the heavily shared exponent bytes do not serialise on one bank.  The
+// selected values are the exact samples the reference's sorted vector holds
+// at those ranks.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+namespace cace {
+
+struct MetricsParams {
+  const double* samples;   // batch sample buffer
+  const int64_t* off;      // [B] first sample of batch scenario b
+  const uint32_t* ncomp;   // [B] completion requests of b's trace
+  const uint32_t* nreq;    // [B] requests of b's trace
+  double* stat;            // [B][2][4]: {p50, p95, p99, max} for TTFT (class 0) and E2E (class 1)
+};
+
+// Zero-based nearest rank of summarize (metrics.cpp:18-22):
+// r = clamp(ceil(q * n), 1, n), the same fp64 operations as the reference.
+__host__ __device__ inline uint32_t nearest_rank0(double q, uint32_t n) {
+  const double r = ceil(q * (double)n);
+  uint64_t ri = r < 1.0 ? 1u : (uint64_t)r;
+  if (ri > n) ri = n;
+  return (uint32_t)(ri - 1);
+}
+
+constexpr int METRICS_BLOCK = 256;
+
+__global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsParams P) {
+  const int seg = blockIdx.x;  // 2 * b + class
+  const int b = seg >> 1, cls = seg & 1;
+  const uint32_t nc = P.ncomp[b], n = P.nreq[b];
+  const uint32_t len = cls ? n - nc : nc;
+  const uint64_t* x = reinterpret_cast<const uint64_t*>(P.samples + P.off[b] + (cls ? nc : 0));
+  double* out = P.stat + (size_t)seg * 4;
+  if (len == 0) {  // compute_run_metrics throws; the host reports it
+    if (threadIdx.x < 4) out[threadIdx.x] = 0.0;
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ uint32_t hist[3][256];
+  __shared__ uint64_t s_prefix[3];
+  __shared__ uint32_t s_krem[3];
+  __shared__ int s_src[3];  // target whose histogram this target shares (distinct prefixes only)
+  __shared__ uint64_t s_max[METRICS_BLOCK / 32];
+
+  // max (the last order statistic) by reduction
+  uint64_t mx = 0;
+  for (uint32_t i = threadIdx.x; i < len; i += METRICS_BLOCK) mx = max(mx, x[i]);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) s_max[warp] = mx;
+  if (threadIdx.x < 3) {
+    const double q = threadIdx.x == 0 ? 0.50 : (threadIdx.x == 1 ? 0.95 : 0.99);
+    s_krem[threadIdx.x] = nearest_rank0(q, len);
+    s_prefix[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t m = s_max[0];
+    for (int w = 1; w < METRICS_BLOCK / 32; ++w) m = max(m, s_max[w]);
+    out[3] = __longlong_as_double((long long)m);
+  }
+
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    const uint64_t mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    if (threadIdx.x < 3) {
+      const int t = threadIdx.x;
+      int src = t;
+      for (int u = 0; u < t; ++u)
+        if (s_prefix[u] == s_prefix[t]) {
+          src = u;
+          break;
+        }
+      s_src[t] = src;
+    }
+    for (int i = threadIdx.x; i < 3 * 256; i += METRICS_BLOCK) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t p0 = s_prefix[0], p1 = s_prefix[1], p2 = s_prefix[2];
+    const bool d1 = s_src[1] == 1, d2 = s_src[2] == 2;  // distinct histograms needed
+    for (uint32_t i0 = 0; i0 < len; i0 += METRICS_BLOCK) {
+      const uint32_t i = i0 + threadIdx.x;
+      const unsigned act = __ballot_sync(0xffffffffu, i < len);
+      if (i < len) {
+        const uint64_t v = x[i];
+        const int d = (int)((v >> shift) & 255u);
+        const uint64_t pv = v & mask;
+        // one histogram per distinct prefix; lanes with the same bin add once
+        const int bin0 = pv == p0 ? d : -1;
+        const int bin1 = d1 && pv == p1 ? d : -1;
+        const int bin2 = d2 && pv == p2 ? d : -1;
+        const int key = (bin0 >= 0 ? bin0 : (bin1 >= 0 ? 256 + bin1 : (bin2 >= 0 ? 512 + bin2 : -1)));
+        const unsigned peers = __match_any_sync(act, key);
+        if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&(&hist[0][0])[key], (uint32_t)__popc(peers));
+      }
+    }
+    __syncthreads();
+    // digit of each target: warp t scans its (shared) histogram
+    if (warp < 3) {
+      const int t = warp;
+      const uint32_t* h = hist[s_src[t]];
+      uint32_t c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = h[lane * 8 + j];
+        sum += c[j];
+      }
+      uint32_t incl = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t excl = incl - sum;
+      const uint32_t k = s_krem[t];
+      if (k >= excl && k < incl) {  // exactly one lane holds rank k's bin
+        uint32_t cum = excl;
+        int d = -1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (d < 0) {
+            if (k < cum + c[j])
+              d = j;
+            else
+              cum += c[j];
+          }
+        }
+        s_krem[t] = k - cum;
+        s_prefix[t] |= (uint64_t)(lane * 8 + d) << shift;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[threadIdx.x] = __longlong_as_double((long long)s_prefix[threadIdx.x]);
+}
+
+}  // namespace cace

@@ -592,6 +592,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (P.dump.decode) P.dump.decode[o] = dc;
       if (P.dump.ttft) P.dump.ttft[o] = ttft;
       if (P.dump.e2e) P.dump.e2e[o] = e2e;
+      // metrics samples (compute_run_metrics, metrics.cpp:44-52): TTFT of
+      // completion requests, then E2E of reasoning requests
+      if (P.dump.samples) {
+        const bool comp = (mc >> 16) == CACE_COMPLETION;
+        P.dump.samples[doff + (comp ? R.ci : P.trace_ncomp[sc.trace] + R.ci)] = comp ? ttft : e2e;
+      }
     }
     // the head leaves the window (collective)
     if (C > 1 && warp_win) win.advance(m, R.nxt, R.nxa);

@@ -19,7 +19,8 @@ struct alignas(16) ReqRec {
   uint32_t nxt;    // next sorted index with the same model (n if none)
   uint32_t mc;     // model | task_class << 16
   double nxa;      // arrival of request nxt (+inf if none)
-  double pad;
+  uint32_t ci;     // index among the trace's requests of the same task class (replay order)
+  uint32_t pad;
 };
 static_assert(sizeof(ReqRec) == 48, "ReqRec layout");
 
@@ -40,6 +41,9 @@ struct DumpDev {
   int32_t* evict_model;
   double* evict_clock;
   int64_t* n_evict;
+  // metrics samples: per dumped scenario, TTFT of its completion requests
+  // then E2E of its reasoning requests, each in replay order, from dump_off
+  double* samples;
 };
 
 struct ReplayParams {

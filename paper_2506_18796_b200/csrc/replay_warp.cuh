@@ -380,6 +380,10 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
       if (P.dump.decode) P.dump.decode[o] = dc;
       if (P.dump.ttft) P.dump.ttft[o] = ttft;
       if (P.dump.e2e) P.dump.e2e[o] = e2e;
+      if (P.dump.samples) {  // metrics samples, as in the lane kernel
+        const bool comp = (mc >> 16) == CACE_COMPLETION;
+        P.dump.samples[doff + (comp ? nc - 1 : P.trace_ncomp[sc.trace] + nr - 1)] = comp ? ttft : e2e;
+      }
     }
     if (need_win) {  // window advance: lanes stride over the models
       __syncwarp();

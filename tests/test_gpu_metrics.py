@@ -1,0 +1,116 @@
+"""GPU parity of the on-device RunMetrics (cace_run_metrics_batch) against the
+reference's compute_run_metrics(run(...)) (metrics.cpp:14-62).
+
+Counts, nearest-rank p50/p95/p99, max, hit rate, load overhead and evictions
+must be bit-identical; the mean divides the replay-order sum while the
+reference sums the sorted samples (metrics.cpp:26), so it is checked to
+1e-12 relative (north_star's latency bar is 1e-9 relative)."""
+import numpy as np
+import pytest
+
+from tests.helpers import bits, ref_catalog, ref_scenario, ref_trace
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2506_18796_b200")
+from paper_2506_18796_b200 import _native as N  # noqa: E402
+from paper_2506_18796_b200 import api, synth  # noqa: E402
+from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig  # noqa: E402
+
+MEAN_RTOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if P.device_count() < 1:
+        pytest.fail("no CUDA device visible: the GPU tests must run on a B200 (no CPU fallback)")
+
+
+def _check(ref, catalog, traces, sc, got, ctx=""):
+    rcat = ref_catalog(ref, catalog)
+    for k in range(len(sc)):
+        want = ref.run_metrics(rcat, ref_trace(traces[int(sc[k]["trace"])]), ref_scenario(ref, sc[k]))
+        g = got[k]
+        c = f"{ctx} scenario {k} {sc[k]}"
+        assert g["status"] == 0, c
+        for f in ("cache_hit_rate", "load_overhead_s", "evictions"):
+            assert bits([g[f]])[0] == bits([want[f]])[0], f"{c} {f}: {g[f]} vs {want[f]}"
+        for lf in ("ttft_completion", "e2e_reasoning"):
+            assert int(g[lf]["count"]) == want[lf]["count"], c
+            for q in ("p50_s", "p95_s", "p99_s", "max_s"):
+                assert bits([g[lf][q]])[0] == bits([want[lf][q]])[0], f"{c} {lf}.{q}: {g[lf][q]!r} vs {want[lf][q]!r}"
+            m, wm = float(g[lf]["mean_s"]), want[lf]["mean_s"]
+            assert abs(m - wm) <= MEAN_RTOL * abs(wm), f"{c} {lf}.mean {m!r} vs {wm!r}"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_run_metrics_random_scenarios(ref, seed):
+    rng = np.random.default_rng(900 + seed)
+    catalog = synth.eight_model_catalog() if seed % 2 == 0 else api.ModelCatalog.build_default()
+    traces = [synth.mixed_trace(catalog, int(n), seed=50 * seed + k, rate=float(r), bursty=bool(k % 2))
+              for k, (n, r) in enumerate([(1, 1.0), (37, 3.0), (2500, 10.0), (6000, 0.5)])]
+    rows = []
+    for _ in range(24):
+        pol = PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.choice([0.0, 0.5, 1.0, 1.7])),
+                           window_length=int(rng.choice([1, 2, 10, 64])),
+                           output_token_normalizer=600, p1_mode=int(rng.integers(0, 2)))
+        cl = ClusterConfig(num_accelerators=int(rng.integers(1, 9)),
+                           unload_time_s=float(rng.choice([0.0, 0.5])))
+        rows.append((int(rng.integers(1, 4)), pol, cl))
+    sc = api.make_scenarios(rows)
+    got, summ = P.run_metrics(traces, catalog, sc, with_summaries=True)
+    _check(ref, catalog, traces, sc, got, f"seed {seed}")
+    # the summaries are the replay's own (bit-identical to run_batch)
+    from tests.helpers import assert_summaries_equal
+
+    assert_summaries_equal(summ, P.run_batch(traces, catalog, sc), "run_metrics summaries")
+
+
+def test_run_metrics_config4_slice(ref):
+    """A slice of the config-4 grid (every variant / window / P1 mode, C 1..8)."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 20_000, seed=1 + s) for s in range(2)]
+    sc = synth.scenario_grid(synth.weight_vectors_cfg3()[::97], range(1, 9), 2,
+                             catalog.max_expected_output_tokens())
+    got = P.run_metrics(traces, catalog, sc)
+    pick = np.random.default_rng(3).choice(len(sc), 40, replace=False)
+    _check(ref, catalog, traces, sc[pick], got[pick], "cfg4 slice")
+
+
+def test_run_metrics_errors_match_reference(ref):
+    """compute_run_metrics' SimErrors (metrics.cpp:37-58): empty report, no
+    completion outcomes, no reasoning outcomes."""
+    catalog = synth.eight_model_catalog()
+    comp = [m for m in range(len(catalog)) if catalog.models[m].task_class == api.TaskClass.COMPLETION]
+    reas = [m for m in range(len(catalog)) if catalog.models[m].task_class == api.TaskClass.REASONING]
+    t_comp = api.Trace(np.arange(5, dtype=float), np.array(comp[:1] * 5), np.full(5, 100), np.full(5, 10))
+    t_reas = api.Trace(np.arange(5, dtype=float), np.array(reas[:1] * 5), np.full(5, 100), np.full(5, 10))
+    t_empty = api.Trace(np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32))
+    traces = [t_comp, t_reas, t_empty]
+    sc = api.make_scenarios([(t, PolicyConfig(), ClusterConfig()) for t in range(3)])
+    got = P.run_metrics(traces, catalog, sc, raise_on_error=False)
+    assert list(got["status"]) == [N.CACE_E_METRICS_NO_E2E, N.CACE_E_METRICS_NO_TTFT, N.CACE_E_METRICS_EMPTY]
+    rcat = ref_catalog(ref, catalog)
+    msgs = []
+    for k in range(3):
+        with pytest.raises(Exception) as ei:
+            ref.run_metrics(rcat, ref_trace(traces[k]), ref_scenario(ref, sc[k]))
+        msgs.append(str(ei.value))
+    for k in range(3):
+        with pytest.raises(api.SimError) as ei:
+            P.run_metrics([traces[k]], catalog, api.make_scenarios([(0, PolicyConfig(), ClusterConfig())]))
+        assert str(ei.value) == msgs[k], (str(ei.value), msgs[k])
+
+
+def test_average_metrics_matches_reference_formula():
+    """average_metrics (metrics.cpp:89-104): elementwise mean in run order."""
+    runs = np.zeros(3, N.METRICS_DTYPE)
+    for i in range(3):
+        runs[i]["cache_hit_rate"] = 0.1 * (i + 1)
+        runs[i]["evictions"] = 10 * i
+        runs[i]["ttft_completion"]["count"] = 5
+        runs[i]["ttft_completion"]["p99_s"] = 1.0 + i
+    avg = P.average_metrics(runs)
+    assert avg["cache_hit_rate"] == ((0.1 + 0.2) + 0.30000000000000004) / 3.0
+    assert avg["evictions"] == 10.0 and avg["ttft_completion"]["count"] == 15
+    assert avg["ttft_completion"]["p99_s"] == 2.0
