@@ -4,6 +4,7 @@
 // (serialize_report, emit_metrics_csv, emit(compare(...))) — byte for byte,
 // the acceptance criterion 9 standard (acceptance.cpp:452-470).
 // Runs on a GPU box; prints one ADAPTER line per check, exits 1 on mismatch.
+#include <cmath>
 #include <cstdio>
 #include <string>
 
@@ -59,6 +60,30 @@ int main() {
     check(a == b, "run_grid byte-identical (" + std::to_string(a.size()) + " bytes, " +
                       std::to_string(cfg->patterns.size() * cfg->variants.size() * cfg->seeds.size()) +
                       " runs)");
+  }
+  // device RunMetrics (run_metrics_many / run_grid_metrics) vs the reference's
+  // compute_run_metrics / average_metrics: exact except the mean (sorted-order
+  // sum in the reference, replay-order sum on the device)
+  for (auto* cfg : {&cmp, &all}) {
+    const GridResult want = run_grid(*cfg, catalog, false);
+    const GridResult got = gpu::run_grid_metrics(*cfg, catalog);
+    bool ok = want.cells.size() == got.cells.size();
+    double worst = 0.0;
+    for (size_t c = 0; ok && c < want.cells.size(); ++c) {
+      const RunMetrics &a = want.cells[c].averaged, &b = got.cells[c].averaged;
+      ok = ok && a.cache_hit_rate == b.cache_hit_rate && a.load_overhead_s == b.load_overhead_s &&
+           a.evictions == b.evictions;
+      for (auto mem : {&RunMetrics::ttft_completion, &RunMetrics::e2e_reasoning}) {
+        const LatencySummary &x = a.*mem, &y = b.*mem;
+        ok = ok && x.count == y.count && x.p50_s == y.p50_s && x.p95_s == y.p95_s &&
+             x.p99_s == y.p99_s && x.max_s == y.max_s;
+        worst = std::max(worst, std::abs(x.mean_s - y.mean_s) / std::max(std::abs(x.mean_s), 1e-300));
+      }
+    }
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.2e", worst);
+    check(ok && worst <= 1e-12, std::string("run_grid_metrics: averaged metrics exact (mean rel diff ") + buf +
+                                    ", " + std::to_string(want.cells.size()) + " cells)");
   }
   // criterion 2 number through the GPU grid
   {

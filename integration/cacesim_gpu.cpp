@@ -150,6 +150,90 @@ SimulationReport run(const Trace& trace, const ModelCatalog& catalog, const Clus
   return run_many({&trace}, catalog, {{policy.config(), cluster}}, {0}).front();
 }
 
+std::vector<RunMetrics> run_metrics_many(const std::vector<const Trace*>& traces,
+                                         const ModelCatalog& catalog,
+                                         const std::vector<std::pair<PolicyConfig, ClusterConfig>>& runs,
+                                         const std::vector<int>& trace_of_run) {
+  for (const auto& [pc, cc] : runs) {  // engine.cpp:79-82, in the reference's order
+    if (pc.window_length < 1) throw SimError("run: window_length must be >= 1");
+    if (cc.num_accelerators < 1) throw SimError("run: need at least one accelerator");
+  }
+  CatalogSoA cat(catalog);
+  std::vector<TraceSoA> tsoa;
+  std::vector<cace_trace_t> tabi;
+  for (const Trace* t : traces) tsoa.emplace_back(*t, catalog);
+  for (const auto& t : tsoa) tabi.push_back(t.abi());
+  const int64_t S = static_cast<int64_t>(runs.size());
+  std::vector<cace_scenario_t> sc;
+  for (int64_t i = 0; i < S; ++i) sc.push_back(scenario(trace_of_run[i], runs[i].first, runs[i].second));
+  std::vector<cace_run_metrics_t> m(S);
+  cace_opts_t opts{0, CACE_KERNEL_AUTO, -1, 0, nullptr};
+  char msg[512] = {0};
+  const int32_t rc = cace_run_metrics_batch(&cat.abi, tabi.data(), static_cast<int32_t>(tabi.size()),
+                                            sc.data(), S, m.data(), nullptr, &opts, msg, sizeof msg);
+  if (rc != CACE_OK) throw SimError(msg);
+  std::vector<RunMetrics> out(S);
+  for (int64_t i = 0; i < S; ++i) {
+    RunMetrics& r = out[i];
+    r.cache_hit_rate = m[i].cache_hit_rate;
+    r.load_overhead_s = m[i].load_overhead_s;
+    r.evictions = m[i].evictions;
+    const cace_latency_summary_t* src[2] = {&m[i].ttft_completion, &m[i].e2e_reasoning};
+    LatencySummary* dst[2] = {&r.ttft_completion, &r.e2e_reasoning};
+    for (int c = 0; c < 2; ++c) {
+      dst[c]->count = static_cast<std::size_t>(src[c]->count);
+      dst[c]->mean_s = src[c]->mean_s;
+      dst[c]->p50_s = src[c]->p50_s;
+      dst[c]->p95_s = src[c]->p95_s;
+      dst[c]->p99_s = src[c]->p99_s;
+      dst[c]->max_s = src[c]->max_s;
+    }
+  }
+  return out;
+}
+
+GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& catalog) {
+  cfg.validate();
+  std::vector<Trace> traces;
+  std::vector<const Trace*> tp;
+  for (PatternName p : cfg.patterns)
+    for (std::uint64_t seed : cfg.seeds)
+      traces.push_back(build_trace(p, cfg.rate, cfg.duration, seed, catalog, cfg.tokens, cfg.windows));
+  for (const auto& t : traces) tp.push_back(&t);
+  std::vector<std::pair<PolicyConfig, ClusterConfig>> runs;
+  std::vector<int> tof;
+  const int ns = static_cast<int>(cfg.seeds.size());
+  for (size_t pi = 0; pi < cfg.patterns.size(); ++pi)
+    for (Variant v : cfg.variants)
+      for (int si = 0; si < ns; ++si) {
+        runs.emplace_back(make_policy_config(cfg, v, catalog), cfg.cluster);
+        tof.push_back(static_cast<int>(pi) * ns + si);
+      }
+  std::vector<RunMetrics> ms = run_metrics_many(tp, catalog, runs, tof);
+  GridResult result;
+  size_t r = 0;
+  for (size_t pi = 0; pi < cfg.patterns.size(); ++pi)
+    for (Variant v : cfg.variants) {
+      GridCell cell;
+      cell.pattern = cfg.patterns[pi];
+      cell.variant = v;
+      std::vector<RunMetrics> per_seed(ms.begin() + r, ms.begin() + r + ns);
+      for (int si = 0; si < ns; ++si) {
+        SimulationReport rep;
+        const Trace& t = traces[pi * ns + si];
+        rep.meta.variant = v;
+        rep.meta.seed = t.seed;
+        rep.meta.pattern = t.pattern;
+        rep.meta.config_hash = config_hash(cfg.cluster, runs[r + si].first);
+        cell.reports.push_back(std::move(rep));
+      }
+      r += ns;
+      cell.averaged = average_metrics(per_seed);
+      result.cells.push_back(std::move(cell));
+    }
+  return result;
+}
+
 GridResult run_grid(const ExperimentConfig& cfg, const ModelCatalog& catalog) {
   cfg.validate();
   // Traces per (pattern, seed), exactly as run_cell builds them (experiment.cpp:74-80).

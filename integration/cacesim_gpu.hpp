@@ -28,4 +28,21 @@ std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
                                        const std::vector<std::pair<PolicyConfig, ClusterConfig>>& runs,
                                        const std::vector<int>& trace_of_run);
 
+// metrics.cpp:35-62 — compute_run_metrics of many replays, computed on the
+// device (cace_run_metrics_batch): no per-request outcomes leave the GPU.
+// Counts, nearest-rank percentiles, max, hit rate, load overhead and
+// evictions are bit-identical to compute_run_metrics(run(...)); mean_s
+// divides the replay-order sum instead of the sorted-order one (~1e-15
+// relative).
+std::vector<RunMetrics> run_metrics_many(const std::vector<const Trace*>& traces,
+                                         const ModelCatalog& catalog,
+                                         const std::vector<std::pair<PolicyConfig, ClusterConfig>>& runs,
+                                         const std::vector<int>& trace_of_run);
+
+// experiment.hpp:54-55 — run_grid whose per-seed metrics come from the
+// device (run_metrics_many) and are averaged with the reference's
+// average_metrics; the cells' reports carry counters and meta but no
+// outcomes (the whole point: 10^11 outcomes never cross PCIe).
+GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& catalog);
+
 }  // namespace cacesim::gpu
