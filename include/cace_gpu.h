@@ -18,6 +18,8 @@
  *   cace_log_selftest        <- the libm log the reference calls             policy.cpp:51
  *   cace_run_metrics_batch   <- RunMetrics compute_run_metrics(const SimulationReport&)
  *                               for every replay of a sweep                 metrics.hpp:29-31
+ *   cace_trace_parse_jsonl   <- Trace parse_trace(const std::string&)        workload.hpp:71
+ *   cace_trace_load_jsonl    <- Trace load_trace(const std::string& path)    workload.hpp:73
  *
  * Error behaviour: every entry returns CACE_OK (0) or one CACE_E_* code per
  * SimError site of the reference, and writes the reference's message text
@@ -56,6 +58,8 @@ enum {
   CACE_E_METRICS_EMPTY = 9, /* "compute_run_metrics: empty report"           metrics.cpp:37-39 */
   CACE_E_METRICS_NO_TTFT = 10, /* "...: no completion outcomes for TTFT"     metrics.cpp:53-55 */
   CACE_E_METRICS_NO_E2E = 11,  /* "...: no reasoning outcomes for E2E"       metrics.cpp:56-58 */
+  CACE_E_PARSE = 12,        /* ParseError of parse_trace (message = its text) workload.cpp:204-266 */
+  CACE_E_IO = 13,           /* "trace: cannot open: <path>"                  workload.cpp:276 */
   CACE_E_INVALID = 20,      /* malformed call (null pointer, bad index, unsupported size) */
   CACE_E_CUDA = 21,         /* CUDA runtime error (message has the CUDA text) */
   CACE_E_NO_DEVICE = 22     /* no CUDA device: there is no CPU fallback */
@@ -217,6 +221,26 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
                                int64_t n_scenarios, cace_run_metrics_t* metrics,
                                cace_summary_t* summaries, const cace_opts_t* opts, char* msg,
                                size_t msg_cap);
+
+/* Trace ingestion: the reference's JSONL trace format (serialize_trace,
+ * workload.cpp:181-202) parsed with parse_trace's semantics and error texts
+ * (workload.cpp:204-266) on all host threads, into an opaque handle whose
+ * columns are copied out as structure-of-arrays.  language / task_class are
+ * the reference's enum codes (types.hpp:23-44); map them to catalog indices
+ * with ModelCatalog::lookup before replay.  JSON syntax errors keep the
+ * reference's "trace line N: invalid JSON: " prefix with this parser's own
+ * description.  No GPU needed. */
+typedef struct cace_trace_jsonl cace_trace_jsonl;
+int32_t cace_trace_parse_jsonl(const char* text, size_t len, cace_trace_jsonl** out, char* msg,
+                               size_t msg_cap);
+int32_t cace_trace_load_jsonl(const char* path, cace_trace_jsonl** out, char* msg, size_t msg_cap);
+int64_t cace_trace_jsonl_size(const cace_trace_jsonl* t);
+void cace_trace_jsonl_header(const cace_trace_jsonl* t, int32_t* pattern, uint64_t* seed,
+                             double* rate, double* duration, int32_t* windows);
+void cace_trace_jsonl_copy(const cace_trace_jsonl* t, uint64_t* request_id, double* arrival,
+                           int32_t* language, int32_t* task_class, int32_t* prompt_tokens,
+                           int32_t* output_tokens);
+void cace_trace_jsonl_free(cace_trace_jsonl* t);
 
 /* Device-resident engine for repeated sweeps (bench, multi-GPU shards):
  * the catalog and traces are uploaded and pre-laid-out once; replays then

@@ -98,6 +98,11 @@ def lib():
         L.ref_run.restype = i32
         L.ref_run.argtypes = [vp, vp, vp, vp, vp, i64, P(RefScenario), P(RefCounters),
                               vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, P(i64), cp, sz]
+        L.ref_parse_trace.restype = i32
+        L.ref_parse_trace.argtypes = [C.c_char_p, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      C.c_char_p, C.c_size_t]
+        L.ref_serialize_built_trace.restype = i64
+        L.ref_serialize_built_trace.argtypes = [i32, C.c_double, C.c_double, C.c_uint64, i32, C.c_char_p, i64]
         L.ref_run_metrics.restype = i32
         L.ref_run_metrics.argtypes = [vp, vp, vp, vp, vp, i64, P(RefScenario), vp, vp, C.c_char_p, C.c_size_t]
         L.ref_dedup_window.restype = i32
@@ -228,6 +233,34 @@ def run(cat: Catalog, trace: dict, sc: RefScenario) -> RefReport:
     return RefReport(cnt.hits, cnt.misses, cnt.evictions, cnt.loads, cnt.load_overhead_s,
                      cnt.max_resident, cold.astype(bool), f["qw"], f["lw"], f["pf"], f["dc"],
                      f["ttft"], f["e2e"], ev_m[:k].copy(), ev_c[:k].copy())
+
+
+def parse_trace(text: bytes) -> dict:
+    """Reference ``parse_trace`` (workload.cpp:204-266); raises RuntimeError
+    with the reference's message."""
+    cap = text.count(b"\n") + 2
+    cols = dict(request_id=np.zeros(cap, np.uint64), arrival=np.zeros(cap), language=np.zeros(cap, np.int32),
+                task_class=np.zeros(cap, np.int32), prompt=np.zeros(cap, np.int32), output=np.zeros(cap, np.int32))
+    n = C.c_int64(0)
+    pat, win = C.c_int32(0), C.c_int32(0)
+    seed = C.c_uint64(0)
+    rate, dur = C.c_double(0), C.c_double(0)
+    msg = C.create_string_buffer(4096)
+    rc = lib().ref_parse_trace(text, len(text), cap, *[_ptr(cols[k]) for k in cols], C.byref(n), C.byref(pat),
+                               C.byref(seed), C.byref(rate), C.byref(dur), C.byref(win), msg, 4096)
+    _check(rc, msg)
+    k = n.value
+    out = {key: v[:k].copy() for key, v in cols.items()}
+    out.update(pattern=pat.value, seed=seed.value, rate=rate.value, duration=dur.value, windows=win.value)
+    return out
+
+
+def serialize_built_trace(pattern: int, rate: float, duration: float, seed: int, windows: int = 1) -> bytes:
+    """serialize_trace(build_trace(...)) with the default catalog and tokens."""
+    n = lib().ref_serialize_built_trace(pattern, rate, duration, seed, windows, None, 0)
+    buf = C.create_string_buffer(int(n))
+    lib().ref_serialize_built_trace(pattern, rate, duration, seed, windows, buf, n)
+    return buf.raw[:n]
 
 
 def run_metrics(cat: Catalog, trace: dict, sc: RefScenario) -> dict:

@@ -352,6 +352,51 @@ int32_t ref_run(void* catp, const double* arrival, const int32_t* model_idx, con
   }
 }
 
+// Reference parse_trace (workload.cpp:204-266): columns of the parsed
+// Trace (up to cap requests) + header; language / task_class as enum codes.
+int32_t ref_parse_trace(const char* text, int64_t len, int64_t cap, uint64_t* request_id,
+                        double* arrival, int32_t* language, int32_t* task_class, int32_t* prompt,
+                        int32_t* output, int64_t* n_out, int32_t* pattern, uint64_t* seed,
+                        double* rate, double* duration, int32_t* windows, char* msg, size_t mcap) {
+  try {
+    Trace t = parse_trace(std::string(text, static_cast<size_t>(len)));
+    *n_out = static_cast<int64_t>(t.requests.size());
+    *pattern = static_cast<int32_t>(t.pattern);
+    *seed = t.seed;
+    *rate = t.arrival_rate_per_s;
+    *duration = t.window_duration_s;
+    *windows = t.windows;
+    for (size_t i = 0; i < t.requests.size() && static_cast<int64_t>(i) < cap; ++i) {
+      const Request& r = t.requests[i];
+      request_id[i] = r.request_id;
+      arrival[i] = r.arrival_time_s;
+      language[i] = static_cast<int32_t>(r.language);
+      task_class[i] = static_cast<int32_t>(r.task_class);
+      prompt[i] = r.prompt_tokens;
+      output[i] = r.output_tokens;
+    }
+    return 0;
+  } catch (const SimError& e) {
+    put_msg(msg, mcap, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_msg(msg, mcap, e.what());
+    return 2;
+  }
+}
+
+// Reference serialize_trace (workload.cpp:181-202) of the trace build_trace
+// generates: writes up to cap bytes, returns the full length.
+int64_t ref_serialize_built_trace(int32_t pattern, double rate, double duration, uint64_t seed,
+                                  int32_t windows, char* out, int64_t cap) {
+  const ModelCatalog cat = ModelCatalog::build_default();
+  Trace t = build_trace(static_cast<PatternName>(pattern), rate, duration, seed, cat, TokenParams{},
+                        windows);
+  const std::string s = serialize_trace(t);
+  if (out && cap > 0) std::memcpy(out, s.data(), std::min<size_t>(s.size(), static_cast<size_t>(cap)));
+  return static_cast<int64_t>(s.size());
+}
+
 // Reference compute_run_metrics (metrics.cpp:35-62) of one run():
 // out = {hit_rate, load_overhead_s, evictions, ttft{mean,p50,p95,p99,max},
 // e2e{mean,p50,p95,p99,max}}, counts = {ttft count, e2e count}.

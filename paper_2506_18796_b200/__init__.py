@@ -26,7 +26,9 @@ from .api import (  # noqa: F401
     dedup_window,
     device_count,
     eviction_score,
+    load_trace,
     make_scenarios,
+    parse_trace,
     run,
     run_batch,
     run_metrics,

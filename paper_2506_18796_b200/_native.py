@@ -28,6 +28,8 @@ CACE_E_DEDUP_LENGTH = 8
 CACE_E_METRICS_EMPTY = 9
 CACE_E_METRICS_NO_TTFT = 10
 CACE_E_METRICS_NO_E2E = 11
+CACE_E_PARSE = 12
+CACE_E_IO = 13
 CACE_E_INVALID = 20
 CACE_E_CUDA = 21
 CACE_E_NO_DEVICE = 22
@@ -127,6 +129,8 @@ EXPORTED = [
     "cace_engine_status_message", "cace_engine_last_launches", "cace_select_victim_batch",
     "cace_eviction_score_batch", "cace_dedup_window_batch", "cace_service_times_batch",
     "cace_log_selftest", "cace_log_host", "cace_probe_log_variant", "cace_run_metrics_batch",
+    "cace_trace_parse_jsonl", "cace_trace_load_jsonl", "cace_trace_jsonl_size", "cace_trace_jsonl_header",
+    "cace_trace_jsonl_copy", "cace_trace_jsonl_free",
 ]
 
 
@@ -147,6 +151,18 @@ def _load():
     L.cace_replay_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, P(DumpABI), P(OptsABI), C.c_char_p, sz]
     L.cace_run_metrics_batch.restype = i32
     L.cace_run_metrics_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, vp, P(OptsABI), C.c_char_p, sz]
+    L.cace_trace_parse_jsonl.restype = i32
+    L.cace_trace_parse_jsonl.argtypes = [C.c_char_p, sz, P(vp), C.c_char_p, sz]
+    L.cace_trace_load_jsonl.restype = i32
+    L.cace_trace_load_jsonl.argtypes = [C.c_char_p, P(vp), C.c_char_p, sz]
+    L.cace_trace_jsonl_size.restype = i64
+    L.cace_trace_jsonl_size.argtypes = [vp]
+    L.cace_trace_jsonl_header.restype = None
+    L.cace_trace_jsonl_header.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.cace_trace_jsonl_copy.restype = None
+    L.cace_trace_jsonl_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.cace_trace_jsonl_free.restype = None
+    L.cace_trace_jsonl_free.argtypes = [vp]
     L.cace_engine_create.restype = i32
     L.cace_engine_create.argtypes = [P(CatalogABI), vp, i32, P(OptsABI), P(vp), C.c_char_p, sz]
     L.cace_engine_destroy.argtypes = [vp]

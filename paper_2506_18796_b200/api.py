@@ -384,6 +384,72 @@ def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray,
     return summ, reports
 
 
+PATTERN_NAMES = ("uniform", "ide-heavy", "popularity-skewed")  # types.cpp:39-46
+
+
+@dataclass
+class TraceHeader:
+    """Trace metadata of the JSONL header (workload.hpp:46-55)."""
+
+    pattern: int
+    seed: int
+    arrival_rate_per_s: float
+    window_duration_s: float
+    windows: int
+
+
+def _trace_from_handle(h, catalog: ModelCatalog):
+    n = int(N.lib.cace_trace_jsonl_size(h))
+    pat, win = C.c_int32(0), C.c_int32(0)
+    seed = C.c_uint64(0)
+    rate, dur = C.c_double(0.0), C.c_double(0.0)
+    N.lib.cace_trace_jsonl_header(h, C.byref(pat), C.byref(seed), C.byref(rate), C.byref(dur), C.byref(win))
+    rid = np.zeros(n, np.uint64)
+    arr = np.zeros(n, np.float64)
+    lang = np.zeros(n, np.int32)
+    cls = np.zeros(n, np.int32)
+    pr = np.zeros(n, np.int32)
+    out = np.zeros(n, np.int32)
+    N.lib.cace_trace_jsonl_copy(h, ptr(rid), ptr(arr), ptr(lang), ptr(cls), ptr(pr), ptr(out))
+    # catalog.lookup(language, task_class) per distinct pair (catalog.cpp:106-116)
+    key = lang.astype(np.int64) * 2 + cls
+    model = np.zeros(n, np.int32)
+    for k in np.unique(key):
+        model[key == k] = catalog.lookup(int(k) // 2, int(k) % 2)
+    hdr = TraceHeader(pat.value, seed.value, rate.value, dur.value, win.value)
+    return Trace(arr, model, pr, out, seed=seed.value), hdr, rid
+
+
+def parse_trace(text, catalog: ModelCatalog):
+    """``parse_trace`` (workload.cpp:204-266) of JSONL text (str or bytes),
+    parsed in native code on all host threads; returns (Trace with catalog
+    indices, TraceHeader, request_id array).  Raises SimError with the
+    reference's ParseError text."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    msg = C.create_string_buffer(4096)
+    rc = N.lib.cace_trace_parse_jsonl(data, len(data), C.byref(h), msg, 4096)
+    if rc != N.CACE_OK:
+        _raise(rc, msg)
+    try:
+        return _trace_from_handle(h, catalog)
+    finally:
+        N.lib.cace_trace_jsonl_free(h)
+
+
+def load_trace(path: str, catalog: ModelCatalog):
+    """``load_trace`` (workload.cpp:274-280): parse_trace of a JSONL file."""
+    h = C.c_void_p()
+    msg = C.create_string_buffer(4096)
+    rc = N.lib.cace_trace_load_jsonl(str(path).encode(), C.byref(h), msg, 4096)
+    if rc != N.CACE_OK:
+        _raise(rc, msg)
+    try:
+        return _trace_from_handle(h, catalog)
+    finally:
+        N.lib.cace_trace_jsonl_free(h)
+
+
 def run_metrics(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray, device: int = 0,
                 raise_on_error: bool = True, kernel: int = KERNEL_AUTO, with_summaries: bool = False):
     """``compute_run_metrics`` (metrics.cpp:35-62) of every scenario's replay,

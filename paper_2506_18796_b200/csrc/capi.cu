@@ -21,6 +21,7 @@
 #include "replay_warp.cuh"
 #include "layout.hpp"
 #include "metrics.cuh"
+#include "trace_jsonl.hpp"
 
 using namespace cace;
 
@@ -850,6 +851,88 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
   cace_engine_destroy(e);
   return rc;
 }
+
+// ---------------- trace ingestion (parse_trace / load_trace) --------------
+
+struct cace_trace_jsonl {
+  ParsedTrace t;
+};
+
+int32_t cace_trace_parse_jsonl(const char* text, size_t len, cace_trace_jsonl** out, char* msg,
+                               size_t msg_cap) {
+  if (!out) return CACE_E_INVALID;
+  *out = nullptr;
+  if (!text && len) return CACE_E_INVALID;
+  try {
+    auto* h = new cace_trace_jsonl();
+    try {
+      h->t = parse_trace_jsonl(text ? text : "", len);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+    return CACE_OK;
+  } catch (const jsonl::TraceError& x) {
+    put_msg(msg, msg_cap, x.what);
+    return CACE_E_PARSE;
+  } catch (const std::exception& x) {
+    put_msg(msg, msg_cap, x.what());
+    return CACE_E_INVALID;
+  }
+}
+
+int32_t cace_trace_load_jsonl(const char* path, cace_trace_jsonl** out, char* msg, size_t msg_cap) {
+  if (!out || !path) return CACE_E_INVALID;
+  *out = nullptr;
+  // load_trace (workload.cpp:274-280)
+  FILE* f = std::fopen(path, "rb");
+  if (!f) {
+    put_msg(msg, msg_cap, std::string("trace: cannot open: ") + path);
+    return CACE_E_IO;
+  }
+  std::string buf;
+  std::fseek(f, 0, SEEK_END);
+  const long sz = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  if (sz > 0) {
+    buf.resize((size_t)sz);
+    const size_t got = std::fread(&buf[0], 1, (size_t)sz, f);
+    buf.resize(got);
+  }
+  std::fclose(f);
+  return cace_trace_parse_jsonl(buf.data(), buf.size(), out, msg, msg_cap);
+}
+
+int64_t cace_trace_jsonl_size(const cace_trace_jsonl* h) {
+  return h ? (int64_t)h->t.arrival.size() : 0;
+}
+
+void cace_trace_jsonl_header(const cace_trace_jsonl* h, int32_t* pattern, uint64_t* seed,
+                             double* rate, double* duration, int32_t* windows) {
+  if (!h) return;
+  if (pattern) *pattern = h->t.pattern;
+  if (seed) *seed = h->t.seed;
+  if (rate) *rate = h->t.rate;
+  if (duration) *duration = h->t.duration;
+  if (windows) *windows = h->t.windows;
+}
+
+void cace_trace_jsonl_copy(const cace_trace_jsonl* h, uint64_t* request_id, double* arrival,
+                           int32_t* language, int32_t* task_class, int32_t* prompt_tokens,
+                           int32_t* output_tokens) {
+  if (!h) return;
+  const ParsedTrace& t = h->t;
+  const size_t n = t.arrival.size();
+  if (request_id && n) std::memcpy(request_id, t.request_id.data(), n * 8);
+  if (arrival && n) std::memcpy(arrival, t.arrival.data(), n * 8);
+  if (language && n) std::memcpy(language, t.language.data(), n * 4);
+  if (task_class && n) std::memcpy(task_class, t.task_class.data(), n * 4);
+  if (prompt_tokens && n) std::memcpy(prompt_tokens, t.prompt.data(), n * 4);
+  if (output_tokens && n) std::memcpy(output_tokens, t.output.data(), n * 4);
+}
+
+void cace_trace_jsonl_free(cace_trace_jsonl* h) { delete h; }
 
 // ---------------- policy-level batch entry points ------------------------
 
