@@ -140,7 +140,25 @@ struct PinnedArena {
     busy = false;
   }
 };
-PinnedArena g_arena;
+PinnedArena g_arena;      // trace-layout staging
+PinnedArena g_arena_out;  // result staging
+
+// Parallel host memcpy (pageable destinations of large results).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const int nth = (int)std::max<size_t>(
+      1, std::min<size_t>(std::max(1u, std::thread::hardware_concurrency()), bytes >> 22));
+  if (nth == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nth; ++w)
+    pool.emplace_back([=] {
+      const size_t b = bytes * w / nth, e = bytes * (w + 1) / nth;
+      std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+    });
+  for (auto& th : pool) th.join();
+}
 
 int g_probe = -2;
 std::mutex g_probe_mu;
@@ -308,20 +326,6 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->segs.clear();
   e->bad_idx.clear();
   e->bad_code.clear();
-  std::vector<int64_t> ok;
-  ok.reserve(n);
-  for (int64_t i = 0; i < n; ++i) {
-    const int32_t st = precheck(e->lay, sc[i]);
-    const bool tv = sc[i].trace >= 0 && sc[i].trace < e->lay.T;
-    const int64_t len = tv ? e->lay.off[sc[i].trace + 1] - e->lay.off[sc[i].trace] : 0;
-    if (st != CACE_OK || len == 0) {
-      e->bad_idx.push_back(i);
-      e->bad_code.push_back(st);
-    } else {
-      ok.push_back(i);
-    }
-  }
-  pt.mark("  precheck");
   auto capof = [&](int64_t i) {
     return (int)((int64_t)sc[i].num_accelerators * sc[i].models_per_accelerator);
   };
@@ -340,56 +344,93 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     const int C = capof(i);
     return use_warp(i) ? 1000 + (C <= 32 ? 1 : 2) : C;
   };
+  // Per scenario, on all host threads: the run() preconditions, the dense
+  // segment key (1..16 lane capacities, 17..18 warp kernel; -1 = invalid) and
+  // a compact coherence key (trace, variant, p1_mode, window).
+  std::vector<int32_t> status(n);
+  std::vector<int8_t> kv(n);
+  std::vector<uint64_t> ck(n);
+  {
+    const int nth = (int)std::max<int64_t>(
+        1, std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), n / 65536));
+    auto work = [&](int w) {
+      for (int64_t i = (int64_t)w * n / nth, ie = (int64_t)(w + 1) * n / nth; i < ie; ++i) {
+        const int32_t st = precheck(e->lay, sc[i]);
+        const bool tv = sc[i].trace >= 0 && sc[i].trace < e->lay.T;
+        const int64_t len = tv ? e->lay.off[sc[i].trace + 1] - e->lay.off[sc[i].trace] : 0;
+        status[i] = st;
+        if (st != CACE_OK || len == 0) {
+          kv[i] = -1;
+          continue;
+        }
+        const int K = key(i);
+        kv[i] = (int8_t)(K >= 1000 ? kMaxLaneC + (K - 1000) : K);
+        const uint32_t win = (uint32_t)std::min(sc[i].window_length, (1 << 27) - 1);
+        ck[i] = ((uint64_t)(uint32_t)sc[i].trace << 32) | ((uint64_t)(sc[i].variant & 7) << 29) |
+                ((uint64_t)(sc[i].p1_mode & 1) << 28) | win;
+      }
+    };
+    if (nth == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (int w = 0; w < nth; ++w) pool.emplace_back(work, w);
+      for (auto& th : pool) th.join();
+    }
+  }
+  pt.mark("  precheck");
   // Coherent warps: segment, then trace, then the control-flow shaping
   // policy fields.  Stable counting sort by segment (O(S)), then each
-  // segment is sorted by (trace, variant, p1_mode, window) unless it already
-  // is (the common case for generated sweeps).
+  // segment is stably sorted by the compact key unless it already is (the
+  // common case for generated sweeps).
+  std::vector<int64_t> ok;
   {
-    std::vector<int> kv(ok.size());
-    int kmax = 0;
-    for (size_t j = 0; j < ok.size(); ++j) {
-      const int K = key(ok[j]);
-      kv[j] = K >= 1000 ? kMaxLaneC + (K - 1000) : K;  // dense: 1..16 lane, 17..18 warp
-      kmax = std::max(kmax, kv[j]);
-    }
+    const int kmax = kMaxLaneC + 2;
     std::vector<int64_t> cnt(kmax + 2, 0);
-    for (int k : kv) ++cnt[k + 1];
+    for (int64_t i = 0; i < n; ++i) {
+      if (kv[i] < 0) {
+        e->bad_idx.push_back(i);
+        e->bad_code.push_back(status[i]);
+      } else {
+        ++cnt[kv[i] + 1];
+      }
+    }
     for (int k = 1; k <= kmax + 1; ++k) cnt[k] += cnt[k - 1];
-    std::vector<int64_t> by_seg(ok.size());
+    ok.resize(cnt[kmax + 1]);
     std::vector<int64_t> start(cnt.begin(), cnt.end());
-    for (size_t j = 0; j < ok.size(); ++j) by_seg[start[kv[j]]++] = ok[j];
-    auto lt = [&](int64_t a, int64_t b) {
-      const cace_scenario_t &x = sc[a], &y = sc[b];
-      if (x.trace != y.trace) return x.trace < y.trace;
-      if (x.variant != y.variant) return x.variant < y.variant;
-      if (x.p1_mode != y.p1_mode) return x.p1_mode < y.p1_mode;
-      return x.window_length < y.window_length;
-    };
+    for (int64_t i = 0; i < n; ++i)
+      if (kv[i] >= 0) ok[start[kv[i]]++] = i;
+    auto lt = [&](int64_t a, int64_t b) { return ck[a] < ck[b]; };
     for (int k = 0; k <= kmax; ++k) {
-      auto b = by_seg.begin() + cnt[k], e2 = by_seg.begin() + cnt[k + 1];
+      auto b = ok.begin() + cnt[k], e2 = ok.begin() + cnt[k + 1];
       if (!std::is_sorted(b, e2, lt)) std::stable_sort(b, e2, lt);
     }
-    ok.swap(by_seg);
   }
   pt.mark("  sort");
   // Lane segments: every (capacity, trace) group is padded to a whole number
   // of warps with shadow lanes (copies of the group's first scenario that
   // write nothing) so each warp is trace-uniform and walks its trace in
   // lockstep.  Warp segments need no padding (one warp = one scenario).
+  // (segment key and trace read from the compact per-scenario arrays)
+  auto seg_of = [&](int64_t i) {
+    const int d = kv[i];
+    return d > kMaxLaneC ? 1000 + (d - kMaxLaneC) : d;
+  };
+  auto trace_of = [&](int64_t i) { return (int32_t)(ck[i] >> 32); };
   std::vector<int64_t> order;
-  order.reserve(ok.size() + 32 * 64);
+  order.reserve(ok.size() + ok.size() / 8 + 32 * 64);
   for (size_t k = 0; k < ok.size();) {
-    const int K = key(ok[k]);
+    const int K = seg_of(ok[k]);
     const int64_t seg_b = (int64_t)order.size();
     size_t j = k;
     if (K >= 1000) {
-      while (j < ok.size() && key(ok[j]) == K) order.push_back(ok[j++]);
+      while (j < ok.size() && seg_of(ok[j]) == K) order.push_back(ok[j++]);
       e->segs.push_back({K - 1000, seg_b, (int64_t)order.size(), true});
     } else {
-      while (j < ok.size() && key(ok[j]) == K) {
-        const int t = sc[ok[j]].trace;
+      while (j < ok.size() && seg_of(ok[j]) == K) {
+        const int32_t t = trace_of(ok[j]);
         size_t g = j;
-        while (g < ok.size() && key(ok[g]) == K && sc[ok[g]].trace == t) order.push_back(ok[g++]);
+        while (g < ok.size() && seg_of(ok[g]) == K && trace_of(ok[g]) == t) order.push_back(ok[g++]);
         const int64_t pad = (32 - (int64_t)(g - j) % 32) % 32;
         for (int64_t q = 0; q < pad; ++q) order.push_back(ok[j] | (int64_t)kShadowBit);
         j = g;
@@ -704,9 +745,18 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       CK(cudaStreamSynchronize(s));
       pt.mark("replay");
     }
+    // summaries: DMA into pinned staging, then a threaded copy to the
+    // caller's (pageable) array; small results go directly
+    const size_t sbytes = (size_t)n_scenarios * sizeof(cace_summary_t);
+    void* stage = sbytes >= ((size_t)8 << 20) ? g_arena_out.acquire(sbytes) : nullptr;
+    struct StageGuard {
+      void* p;
+      ~StageGuard() {
+        if (p) g_arena_out.release();
+      }
+    } sguard{stage};
     if (n_scenarios > 0)
-      CK(cudaMemcpyAsync(summaries, d_out.p, n_scenarios * sizeof(cace_summary_t),
-                         cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(stage ? stage : summaries, d_out.p, sbytes, cudaMemcpyDeviceToHost, s));
     if (nd > 0) {
       auto back = [&](void* h, const void* d, size_t bytes) {
         if (h && d && bytes) CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
@@ -723,6 +773,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       back(dump->n_evict, d_nev.p, (size_t)nd * 8);
     }
     CK(cudaStreamSynchronize(s));
+    if (stage) par_memcpy(summaries, stage, sbytes);
     pt.mark("download");
     for (int64_t i = 0; i < n_scenarios; ++i) {
       if (summaries[i].status != CACE_OK) {
