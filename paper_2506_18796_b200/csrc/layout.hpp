@@ -184,7 +184,8 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
       r.mc = (uint32_t)m | ((uint32_t)(cat.cls[m] == CACE_REASONING) << 16);
       // same-class requests after k (turned into the class-local index below)
       r.ci = cat.cls[m] == CACE_REASONING ? (uint32_t)(n - 1 - k) - ncomp : ncomp;
-      r.pad = 0;
+      r.prv = 0xffffffffu;
+      if (last[m] < (uint32_t)n) rec[b + last[m]].prv = (uint32_t)k;
       worst = std::max(worst, r.prefill + r.decode);
       last[m] = (uint32_t)k;
       L.perm[b + k] = i;

@@ -20,7 +20,7 @@ struct alignas(16) ReqRec {
   uint32_t mc;     // model | task_class << 16
   double nxa;      // arrival of request nxt (+inf if none)
   uint32_t ci;     // index among the trace's requests of the same task class (replay order)
-  uint32_t pad;
+  uint32_t prv;    // previous sorted index with the same model (0xffffffff if none)
 };
 static_assert(sizeof(ReqRec) == 48, "ReqRec layout");
 

@@ -13,8 +13,14 @@
 //     (policy.cpp:39-78, glibc-log P1) is computed by its owner lane in
 //     parallel, then "first strict max in (last_used, model_id) order"
 //     (policy.cpp:92-113) is a warp reduction (no fp32 screening needed).
-// The lookahead window (first[m], rank[m]) lives in shared memory per warp and
-// is advanced cooperatively (lanes stride over models, ballot/popc).
+// The lookahead window: first[m] and the arrival time of that request live in
+// shared memory per warp.  For windows of <= 1024 requests the ranks come
+// from a sliding 1024-bit map of "first pending occurrence" positions (lane l
+// holds positions k + 32 l .. k + 32 l + 31; one funnel shift per request),
+// so rank(m) = popcount of the map below first[m] is a warp prefix sum at
+// decision time and nothing per model is touched per request.  Longer
+// windows keep explicit ranks advanced cooperatively (lanes stride over
+// models, ballot/popc).
 // Scenario-level state (cursor, counters, fingerprints) is warp-uniform:
 // every lane computes it identically; lane 0 writes the summary.
 #pragma once
@@ -29,6 +35,8 @@
 namespace cace {
 
 constexpr int WARP_BLOCK = 128;  // 4 scenarios per block
+// catalog columns at the start of the warp kernel's shared memory (8-aligned)
+inline __host__ __device__ size_t warp_smem_cat(int M) { return ((size_t)M * (3 * 8 + 4) + 7) & ~(size_t)7; }
 
 // Order-preserving unsigned key of a non-NaN double (-0.0 folded onto +0.0,
 // which compare equal in the reference's doubles).
@@ -57,7 +65,9 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   double* s_p2 = s_lt + M;
   double* s_tok = s_p2 + M;
   int* s_lex = reinterpret_cast<int*>(s_tok + M);
-  uint32_t* wfirst = reinterpret_cast<uint32_t*>(s_lex + M);  // [4][M]
+  double* wfa = reinterpret_cast<double*>(smem + warp_smem_cat(M));  // [4][M] arrival of first[m]
+  double* wp4 = wfa + (size_t)(WARP_BLOCK / 32) * M;                  // [4][M] exact p4 of model m
+  uint32_t* wfirst = reinterpret_cast<uint32_t*>(wp4 + (size_t)(WARP_BLOCK / 32) * M);  // [4][M]
   uint32_t* wrank = wfirst + (size_t)(WARP_BLOCK / 32) * M;   // [4][M]
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
@@ -85,6 +95,12 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   const double norm = (double)sc.output_token_normalizer;
   uint32_t* first = wfirst + (size_t)warp * M;
   uint32_t* rank = wrank + (size_t)warp * M;
+  double* fa = wfa + (size_t)warp * M;
+  double* p4t = wp4 + (size_t)warp * M;
+  // exact p4 of every model (policy.cpp:66-67), once per scenario
+  for (int m = lane; m < M; m += 32) p4t[m] = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (s_tok[m] / norm);
+  const bool bitmap = need_win && w <= 1024;  // rank from the first-occurrence map
+  uint32_t fo = 0;  // this lane's 32 positions of the map
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -94,13 +110,24 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   }
   if (need_win) {
     const uint32_t* f0 = P.first0 + (int64_t)sc.trace * M;
-    for (int m = lane; m < M; m += 32) first[m] = __ldg(f0 + m);
-    __syncwarp();
     for (int m = lane; m < M; m += 32) {
-      const uint32_t fm = first[m];
-      uint32_t c = 0;
-      for (int q = 0; q < M; ++q) c += first[q] < fm ? 1u : 0u;
-      rank[m] = c;
+      first[m] = __ldg(f0 + m);
+      fa[m] = first[m] < n ? __ldg(&tr[first[m]].arrival) : INFINITY;
+    }
+    __syncwarp();
+    if (bitmap) {
+      // positions [0, 1024): first occurrences in the trace
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t pos = 32u * lane + b;
+        if (pos < n && __ldg(&tr[pos].prv) == 0xffffffffu) fo |= 1u << b;
+      }
+    } else {
+      for (int m = lane; m < M; m += 32) {
+        const uint32_t fm = first[m];
+        uint32_t c = 0;
+        for (int q = 0; q < M; ++q) c += first[q] < fm ? 1u : 0u;
+        rank[m] = c;
+      }
     }
     __syncwarp();
   }
@@ -133,6 +160,13 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
     const double a = na, pf = npf, dc = ndc;
     const uint32_t nxt = nnxt, mc = nmc;
     if (k + 1 < n) load_rec(tr + k + 1, na, npf, ndc, nnxt, nmc);
+    // window maintenance inputs, needed only at the end of the iteration
+    double nxa = 0.0;
+    uint32_t eprv = 0u;
+    if (need_win) {
+      nxa = __ldg(&tr[k].nxa);
+      if (bitmap && k + 1024 < n) eprv = __ldg(&tr[k + 1024].prv);
+    }
     const int m = (int)(mc & 0xffffu);
 
     if (!(a < cur.t)) {  // head's Arrival into an empty queue
@@ -223,6 +257,37 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
         } else {
           // ---- eviction decision: each lane scores its idle slots ----
           const double now = cur.t;
+          // window position of each own slot's model (policy.cpp:57-64):
+          // rank when its first pending request is in [k, min(k + w,
+          // arrived)), else -1 (collective: the map prefix is warp-wide)
+          int wrk[SPL];
+          uint32_t excl = 0;
+          if (bitmap) {
+            const uint32_t pc = __popc(fo);
+            uint32_t incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(kFull, incl, o);
+              if (lane >= o) incl += y;
+            }
+            excl = incl - pc;
+          }
+#pragma unroll
+          for (int j = 0; j < SPL; ++j) {
+            wrk[j] = -1;
+            const bool cand = need_win && svalid[j] && !sbusy[j];
+            const int ms = cand ? smodel[j] : 0;
+            const uint32_t fm = cand ? first[ms] : k;
+            const bool iw = cand && fm - k < w && fa[ms] < now;
+            if (bitmap) {
+              const uint32_t d = iw ? fm - k : 0u;  // < 1024
+              const uint32_t wl = __shfl_sync(kFull, fo, (int)(d >> 5));
+              const uint32_t el = __shfl_sync(kFull, excl, (int)(d >> 5));
+              if (iw) wrk[j] = (int)(el + __popc(wl & ((1u << (d & 31u)) - 1u)));
+            } else if (iw) {
+              wrk[j] = (int)rank[ms];
+            }
+          }
           // Per lane: the best own candidate by (total desc, last_used asc,
           // lex asc) over non-NaN totals, its own sorted-first by
           // (last_used, lex), and whether any own total is NaN.
@@ -251,13 +316,8 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             }
             const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[ms];
             double p3 = 0.0;
-            if (variant != CACE_MINUS_P3) {
-              const uint32_t fm = first[ms];
-              bool iw = fm < n && fm - k < w;
-              if (iw) iw = __ldg(&tr[fm].arrival) < now;
-              p3 = iw ? (double)rank[ms] / wd : 1.0;
-            }
-            const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (s_tok[ms] / norm);
+            if (variant != CACE_MINUS_P3) p3 = wrk[j] >= 0 ? (double)wrk[j] / wd : 1.0;
+            const double p4 = p4t[ms];
             const double T = ((p1 + p2) + p3) + p4;
             tnan[j] = T != T;
             has_nan |= tnan[j];
@@ -385,7 +445,22 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
         P.dump.samples[doff + (comp ? nc - 1 : P.trace_ncomp[sc.trace] + nr - 1)] = comp ? ttft : e2e;
       }
     }
-    if (need_win) {  // window advance: lanes stride over the models
+    if (bitmap) {
+      // the window slides to k + 1: position k leaves, k + 1024 enters (a
+      // first occurrence iff its model's previous request is <= k), and the
+      // head's model's next request becomes its first pending occurrence
+      const uint32_t nw = __shfl_down_sync(kFull, fo, 1);
+      fo = __funnelshift_r(fo, lane == 31 ? 0u : nw, 1);
+      if (lane == 31 && k + 1024 < n && eprv + 1u <= k + 1u) fo |= 1u << 31;
+      const uint32_t dj = nxt - (k + 1);
+      if (nxt < n && dj < 1024u && (int)(dj >> 5) == lane) fo |= 1u << (dj & 31u);
+      __syncwarp();
+      if (lane == 0) {
+        first[m] = nxt;
+        fa[m] = nxa;
+      }
+      __syncwarp();
+    } else if (need_win) {  // window advance: lanes stride over the models
       __syncwarp();
       uint32_t cnt = 0;
       for (int b0 = 0; b0 < M; b0 += 32) {
@@ -398,6 +473,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
       if (lane == 0) {
         first[m] = nxt;
         rank[m] = cnt;
+        fa[m] = nxa;
       }
       __syncwarp();
     }
@@ -425,7 +501,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
 }
 
 inline size_t warp_smem_bytes(int M) {
-  return (size_t)M * (3 * 8 + 4) + (size_t)(WARP_BLOCK / 32) * M * 8;
+  return warp_smem_cat(M) + (size_t)(WARP_BLOCK / 32) * M * (8 + 8 + 4 + 4);
 }
 
 }  // namespace cace

@@ -38,9 +38,11 @@ def test_forced_warp_kernel_vs_reference(ref, seed):
     assert_summaries_equal(summ, lane, "warp vs lane")
 
 
-@pytest.mark.parametrize("cap", [32, 48])
-def test_config5_shape_vs_port(cap):
-    """256 CodeLLMs, bursty trace, window 1024, capacity 32/48 (SPL 1/2)."""
+@pytest.mark.parametrize("cap,windows", [(32, (16, 256, 1024)), (48, (16, 256, 1024)),
+                                         (32, (1000, 1024, 1025, 3000)), (40, (1, 1023, 2048))])
+def test_config5_shape_vs_port(cap, windows):
+    """256 CodeLLMs, bursty trace, capacity 32/48 (SPL 1/2); windows up to
+    1024 use the first-occurrence bitmap, longer ones explicit ranks."""
     import paper_2506_18796_b200 as P
     from oracle import port
     from paper_2506_18796_b200 import api, synth
@@ -52,7 +54,7 @@ def test_config5_shape_vs_port(cap):
     rows = []
     for i in range(24):
         pol = PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.uniform(0, 2)),
-                           window_length=int(rng.choice([16, 256, 1024])), p1_mode=int(rng.integers(0, 2)))
+                           window_length=int(rng.choice(windows)), p1_mode=int(rng.integers(0, 2)))
         rows.append((i % 2, pol, ClusterConfig(num_accelerators=cap)))
     sc = api.make_scenarios(rows)
     got = P.run_batch(traces, catalog, sc)
