@@ -35,6 +35,7 @@ __host__ __device__ inline uint32_t nearest_rank0(double q, uint32_t n) {
 }
 
 constexpr int METRICS_BLOCK = 256;
+constexpr int METRICS_LIST = 5120;  // keys kept in shared memory once the prefixes are narrow
 
 __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsParams P) {
   const int seg = blockIdx.x;  // 2 * b + class
@@ -51,8 +52,11 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
   __shared__ uint32_t hist[3][256];
   __shared__ uint64_t s_prefix[3];
   __shared__ uint32_t s_krem[3];
+  __shared__ uint32_t s_cnt[3];  // keys under each target's prefix
   __shared__ int s_src[3];  // target whose histogram this target shares (distinct prefixes only)
   __shared__ uint64_t s_max[METRICS_BLOCK / 32];
+  __shared__ uint64_t s_list[METRICS_LIST];  // keys matching a target prefix (after compaction)
+  __shared__ uint32_t s_nlist;
 
   // max (the last order statistic) by reduction
   uint64_t mx = 0;
@@ -71,8 +75,35 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
     out[3] = __longlong_as_double((long long)m);
   }
 
+  // The passes read the segment from global memory until the targets'
+  // prefixes are narrow enough that every key matching one of them fits in
+  // shared memory; those keys are then compacted once and the remaining
+  // passes run on the shared list.
+  const uint64_t* src = x;
+  uint32_t slen = len;
+  bool compacted = false;
   for (int shift = 56; shift >= 0; shift -= 8) {
     const uint64_t mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    if (!compacted && shift <= 40) {
+      // total keys under the (distinct) current prefixes = the selected bins
+      // of the previous pass: compact if they fit
+      if (threadIdx.x == 0) s_nlist = 0;
+      __syncthreads();
+      const uint64_t r0 = s_prefix[0], r1 = s_prefix[1], r2 = s_prefix[2];
+      const uint32_t need = s_cnt[0] + (r1 != r0 ? s_cnt[1] : 0u) + (r2 != r0 && r2 != r1 ? s_cnt[2] : 0u);
+      if (need <= (uint32_t)METRICS_LIST) {
+        const uint64_t q0 = s_prefix[0], q1 = s_prefix[1], q2 = s_prefix[2];
+        for (uint32_t i = threadIdx.x; i < len; i += METRICS_BLOCK) {
+          const uint64_t v = x[i];
+          const uint64_t pv = v & mask;
+          if (pv == q0 || pv == q1 || pv == q2) s_list[atomicAdd(&s_nlist, 1u)] = v;
+        }
+        __syncthreads();
+        src = s_list;
+        slen = s_nlist;
+        compacted = true;
+      }
+    }
     if (threadIdx.x < 3) {
       const int t = threadIdx.x;
       int src = t;
@@ -87,11 +118,11 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
     __syncthreads();
     const uint64_t p0 = s_prefix[0], p1 = s_prefix[1], p2 = s_prefix[2];
     const bool d1 = s_src[1] == 1, d2 = s_src[2] == 2;  // distinct histograms needed
-    for (uint32_t i0 = 0; i0 < len; i0 += METRICS_BLOCK) {
+    for (uint32_t i0 = 0; i0 < slen; i0 += METRICS_BLOCK) {
       const uint32_t i = i0 + threadIdx.x;
-      const unsigned act = __ballot_sync(0xffffffffu, i < len);
-      if (i < len) {
-        const uint64_t v = x[i];
+      const unsigned act = __ballot_sync(0xffffffffu, i < slen);
+      if (i < slen) {
+        const uint64_t v = src[i];
         const int d = (int)((v >> shift) & 255u);
         const uint64_t pv = v & mask;
         // one histogram per distinct prefix; lanes with the same bin add once
@@ -135,6 +166,7 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
         }
         s_krem[t] = k - cum;
         s_prefix[t] |= (uint64_t)(lane * 8 + d) << shift;
+        s_cnt[t] = c[d];  // keys under the extended prefix
       }
     }
     __syncthreads();

@@ -331,9 +331,16 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
+  bool dump_outcomes = false;
+  double* samples = nullptr;  // this scenario's metrics samples
+  uint32_t ncomp_t = 0;
   if (DUMP && !shadow) {
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
+    dump_outcomes = P.dump.cold || P.dump.queue_wait || P.dump.load_wait || P.dump.prefill ||
+                    P.dump.decode || P.dump.ttft || P.dump.e2e;
+    if (dslot >= 0 && P.dump.samples) samples = P.dump.samples + doff;
+    ncomp_t = P.trace_ncomp[sc.trace];
   }
   RecStream rs;
   rs.init(tr, n, S.rec);
@@ -584,19 +591,21 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     }
     ho = hmix(ho, dbits(ttft) ^ (hit ? 0ull : 1ull));
     if (DUMP && dslot >= 0) {
-      const int64_t o = doff + P.perm[base + k];
-      if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
-      if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - lw;
-      if (P.dump.load_wait) P.dump.load_wait[o] = lw;
-      if (P.dump.prefill) P.dump.prefill[o] = pf;
-      if (P.dump.decode) P.dump.decode[o] = dc;
-      if (P.dump.ttft) P.dump.ttft[o] = ttft;
-      if (P.dump.e2e) P.dump.e2e[o] = e2e;
+      if (dump_outcomes) {  // per-request outcomes in the caller's request order
+        const int64_t o = doff + P.perm[base + k];
+        if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
+        if (P.dump.queue_wait) P.dump.queue_wait[o] = qd - lw;
+        if (P.dump.load_wait) P.dump.load_wait[o] = lw;
+        if (P.dump.prefill) P.dump.prefill[o] = pf;
+        if (P.dump.decode) P.dump.decode[o] = dc;
+        if (P.dump.ttft) P.dump.ttft[o] = ttft;
+        if (P.dump.e2e) P.dump.e2e[o] = e2e;
+      }
       // metrics samples (compute_run_metrics, metrics.cpp:44-52): TTFT of
       // completion requests, then E2E of reasoning requests
-      if (P.dump.samples) {
+      if (samples) {
         const bool comp = (mc >> 16) == CACE_COMPLETION;
-        P.dump.samples[doff + (comp ? R.ci : P.trace_ncomp[sc.trace] + R.ci)] = comp ? ttft : e2e;
+        samples[comp ? R.ci : ncomp_t + R.ci] = comp ? ttft : e2e;
       }
     }
     // the head leaves the window (collective)
