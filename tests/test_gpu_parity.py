@@ -148,6 +148,22 @@ def test_error_paths_match_reference_messages(ref):
         assert str(ei.value) == str(er.value)
 
 
+def test_domain_rejections():
+    """Inputs outside the engine's domain fail loudly with CACE_E_INVALID
+    (DESIGN.md section 7): negative arrivals (parse_trace rejects them,
+    workload.cpp:245-248), negative prompt tokens, negative unload time."""
+    catalog = synth.eight_model_catalog()
+    good = synth.mixed_trace(catalog, 50, seed=3)
+    neg = api.Trace(good.arrival_time_s - 1.0, good.model, good.prompt_tokens, good.output_tokens)
+    with pytest.raises(api.SimError, match="negative arrival_time_s"):
+        P.run(neg, catalog)
+    badp = api.Trace(good.arrival_time_s, good.model, -good.prompt_tokens, good.output_tokens)
+    with pytest.raises(api.SimError, match="negative prompt_tokens"):
+        P.run(badp, catalog)
+    with pytest.raises(api.SimError, match="unload_time_s"):
+        P.run(good, catalog, ClusterConfig(unload_time_s=-1.0))
+
+
 def test_empty_trace(ref):
     catalog = synth.eight_model_catalog()
     t = api.Trace(np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.int32))
