@@ -88,6 +88,20 @@ __device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
 __device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
 __device__ __forceinline__ bool is_idle(double st) { return __double2hiint(st) >= 0; }
 
+// Number of Busy slots (sign bits), summed as a balanced tree so the count
+// is not a C-deep dependency chain.
+template <int C>
+__device__ __forceinline__ int busy_count(const double (&st)[C]) {
+  int b[C];
+#pragma unroll
+  for (int s = 0; s < C; ++s) b[s] = (int)((unsigned)__double2hiint(st[s]) >> 31);
+#pragma unroll
+  for (int w = 1; w < C; w *= 2)
+#pragma unroll
+    for (int s = 0; s + w < C; s += 2 * w) b[s] += b[s + w];
+  return b[0];
+}
+
 // Event key (time, kind, seq) of engine.cpp:49-55.
 struct Cursor {
   double t;
@@ -162,6 +176,13 @@ struct Window {
     }
   }
   WinEnt gather(int ms) const { return WinEnt{f[ms], (float)r[ms], fa[ms]}; }
+  int pmk = 0;
+  uint32_t pnx = 0;
+  void prepare(int mk, uint32_t nx) {
+    pmk = mk;
+    pnx = nx;
+  }
+  void commit(double nxa) { advance(pmk, pnx, nxa); }
   void advance(int mk, uint32_t nx, double nxa) {
     uint32_t cnt = 0;
     for (int j = 0; j < M; ++j)
@@ -195,25 +216,39 @@ struct Window {
   }
   // Per lane (no collective): model ms's entry.
   __device__ __forceinline__ WinEnt gather(int ms) const { return tab[ms]; }
-  // Collective: the head (model mk) is served; mk's first becomes nx (arrival nxa).
-  __device__ __forceinline__ void advance(int mk, uint32_t nx, double nxa) {
+  // Collective, split so the ballot/popc latency overlaps the request's own
+  // dependency chain: prepare (top of the iteration) computes the state after
+  // the head (model mk) is served -- mk's first becomes nx -- without
+  // touching what this iteration's decisions read; commit (end) installs it.
+  uint32_t nf[MW], nr[MW];
+  int pmk;
+  __device__ __forceinline__ void prepare(int mk, uint32_t nx) {
     const int lane = threadIdx.x & 31;
+    pmk = mk;
     uint32_t cnt = 0;
 #pragma unroll
     for (int q = 0; q < MW; ++q) {
       const int m = lane + 32 * q;
       const bool before = m < M && m != mk && f[q] < nx;
       cnt += __popc(__ballot_sync(kFull, before));
-      if (before) r[q] -= 1;
+      nf[q] = f[q];
+      nr[q] = before ? r[q] - 1 : r[q];
     }
+#pragma unroll
+    for (int q = 0; q < MW; ++q)
+      if (lane + 32 * q == mk) {
+        nf[q] = nx;
+        nr[q] = cnt;
+      }
+  }
+  __device__ __forceinline__ void commit(double nxa) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int q = 0; q < MW; ++q) {
       const int m = lane + 32 * q;
-      if (m == mk) {
-        f[q] = nx;
-        r[q] = cnt;
-        tab[m].fa = nxa;
-      }
+      f[q] = nf[q];
+      r[q] = nr[q];
+      if (m == pmk) tab[m].fa = nxa;
       if (m < M) *reinterpret_cast<uint2*>(&tab[m]) = make_uint2(f[q], __float_as_uint((float)r[q]));
     }
     __syncwarp();
@@ -387,9 +422,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 
     // classify (engine.cpp:163-173): resident (never Loading here) -> hit
     int hs = (int)S.slot_of[m * st] - 1;
-    int nbusy = 0;
-#pragma unroll
-    for (int s = 0; s < C; ++s) nbusy += (int)((unsigned)__double2hiint(stime[s]) >> 31);
+    const int nbusy = busy_count<C>(stime);
     const bool decide = hs < 0 && occ == C && C - nbusy >= 2;
 
     double lw = 0.0;
@@ -401,7 +434,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       // register read).
       const double td = S.done[hs * st];
       const uint32_t tq = S.seq[hs * st];
-      if (td > cur.t || (td == cur.t && (cur.kind == 0 || (cur.kind == 1 && tq > cur.seq)))) {
+      // predicates evaluated side by side (no short-circuit chain behind the loads)
+      const bool tie_busy = (cur.kind == 0) | ((cur.kind == 1) & (tq > cur.seq));
+      if ((td > cur.t) | ((td == cur.t) & tie_busy)) {
         // Busy: blocked until the model's own ServiceComplete (td, 1, tq).
         // Completions with key <= it become Idle: done < td, and equal
         // times break ties on the push seq.
@@ -608,8 +643,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         samples[comp ? R.ci : ncomp_t + R.ci] = comp ? ttft : e2e;
       }
     }
-    // the head leaves the window (collective)
-    if (C > 1 && warp_win) win.advance(m, R.nxt, R.nxa);
+    if (C > 1 && warp_win) {  // the head leaves the window (collective)
+      win.prepare(m, R.nxt);
+      win.commit(R.nxa);
+    }
   }
   }
 
