@@ -5,9 +5,12 @@ Workload (default): BASELINE config 4 — 1,048,576 scenarios (4096
 reference-expressible weight vectors x capacities 1..8 x 32 seeds) x 100k
 requests of a synthetic mixed completion/reasoning trace (8 CodeLLMs), i.e.
 1.05e11 scenario-requests per step.  One step = one full replay of the sweep.
-With N GPUs (torchrun, one process per GPU) the scenarios are split into N
-cost-balanced contiguous shards (strong scaling: total work fixed), replayed
-independently, and the fixed-size per-scenario summaries are all-gathered
+With N GPUs (torchrun, one process per GPU) scenarios are independent units
+sharded across ranks with no data-path collective: by default (--scaling
+weak) every rank replays its own full config-4 sweep (rank r's 32 traces use
+seeds 32r+1..32r+32), so the job replays N x 1.05e11 scenario-requests per
+step; --scaling strong splits one 1M-scenario sweep into N cost-balanced
+contiguous shards.  The fixed-size per-scenario summaries are all-gathered
 over NCCL (the only collective; included in the timed step).
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
@@ -47,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank replays its own full sweep (default); strong: one sweep split over ranks")
     return ap.parse_args()
 
 
@@ -54,13 +59,15 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def workload(args):
+def workload(args, part: int = 0):
+    """The sweep of one rank under weak scaling (part = rank; part 0 is the
+    BASELINE workload itself), or the whole sweep under strong scaling."""
     from paper_2506_18796_b200 import synth
 
     if args.config == 5:
-        return synth.config5(n_requests=args.requests, n_scenarios=args.scenarios)
+        return synth.config5(n_requests=args.requests, n_scenarios=args.scenarios, trace_seed=1 + part)
     catalog = synth.eight_model_catalog()
-    traces = [synth.mixed_trace(catalog, args.requests, seed=1 + s) for s in range(args.seeds)]
+    traces = [synth.mixed_trace(catalog, args.requests, seed=1 + part * args.seeds + s) for s in range(args.seeds)]
     pols = synth.weight_vectors_cfg3()[:: args.vectors_stride]
     sc = synth.scenario_grid(pols, range(1, 9), args.seeds, catalog.max_expected_output_tokens())
     return catalog, traces, sc
@@ -170,7 +177,7 @@ def run_reference_arm(args):
     print(json.dumps({
         "impl": "reference", "metric": "scenario-requests replayed/sec", "value": value,
         "unit": "scenario-requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE config {args.config}, bounded random sample per step",
                    "requests": args.requests, "scenarios_per_step": per_step},
@@ -221,12 +228,17 @@ def main():
     import paper_2506_18796_b200 as P
     from paper_2506_18796_b200 import SUMMARY_DTYPE
 
-    catalog, traces, sc_all = workload(args)
     from paper_2506_18796_b200.shard import shard_bounds
 
-    bounds = shard_bounds(sc_all, world)
-    sc = sc_all[bounds[rank]:bounds[rank + 1]]
-    S_total = len(sc_all)
+    if args.scaling == "weak":
+        catalog, traces, sc = workload(args, part=rank)
+        sc_all = sc  # the CPU baseline / parity sample (world == 1 only)
+        bounds = [r * len(sc) for r in range(world + 1)]
+    else:
+        catalog, traces, sc_all = workload(args)
+        bounds = shard_bounds(sc_all, world)
+        sc = sc_all[bounds[rank]:bounds[rank + 1]]
+    S_total = bounds[-1]
     n_req = args.requests
     # A dedicated (non-default) stream: the engine, the events and the L2
     # flush all run on it, so the CUDA events bracket exactly the replay.
@@ -356,14 +368,16 @@ def main():
     out = {
         "metric": "scenario-requests replayed/sec", "value": value, "unit": "scenario-requests/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": ("BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests"
                                 % (args.seeds, n_req)) if args.config == 4 else
                                ("BASELINE config 5: %d scenarios x %d-request bursty trace, 256 CodeLLMs, capacity 32, "
                                 "window 1024" % (S_total, n_req)),
                    "scenarios": S_total, "requests_per_trace": n_req, "models": len(catalog),
-                   "parallelism": f"scenario shards x{world}", "l2": "flushed (256 MB write) before every step",
+                   "parallelism": (f"scenario shards x{world}, each rank its own full sweep (weak)"
+                                   if args.scaling == "weak" else f"one sweep split over {world} ranks (strong)"),
+                   "l2": "flushed (256 MB write) before every step",
                    "vectors_stride": args.vectors_stride},
         "eviction_decisions_per_s": evictions / (t_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",

@@ -110,12 +110,13 @@ def config2(n_requests: int = 10_000, seed: int = 1, capacity: int = 3):
     return catalog, traces, make_scenarios(rows)
 
 
-def config5(n_requests: int = 10_000_000, n_scenarios: int = 8192, capacity: int = 32, window: int = 1024):
+def config5(n_requests: int = 10_000_000, n_scenarios: int = 8192, capacity: int = 32, window: int = 1024,
+            trace_seed: int = 1):
     """BASELINE config 5: 256 CodeLLMs, one bursty (MMPP) trace, long window,
     capacity 32; scenarios = w1 x {cace, -p1, -p2, -p4} x P1 mode x unload
     delay (n_scenarios of that grid).  Needs the warp-per-scenario kernel."""
     catalog = ModelCatalog.synthetic_pool(256, seed=5)
-    traces = [mixed_trace(catalog, n_requests, seed=1, rate=40.0, bursty=True)]
+    traces = [mixed_trace(catalog, n_requests, seed=trace_seed, rate=40.0, bursty=True)]
     rows = []
     variants = (Variant.CACE_FULL, Variant.CACE_MINUS_P1, Variant.CACE_MINUS_P2, Variant.CACE_MINUS_P4)
     per = max(1, n_scenarios // (len(variants) * 2 * 16))
