@@ -708,13 +708,17 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       d_doff.upload(doff.data(), doff.size(), s);
       dd.slot = d_slot.p;
       dd.dump_off = d_doff.p;
+      // dump buffers start zeroed: eviction logs are written only up to
+      // each scenario's eviction count, and the whole arrays are copied back
       auto mk = [&](DBuf<double>& b, double* h) -> double* {
         if (!h) return nullptr;
         b.alloc(total, s);
+        if (total) CK(cudaMemsetAsync(b.p, 0, total * sizeof(double), s));
         return b.p;
       };
       if (dump->cold_start) {
         d_cold.alloc(total, s);
+        if (total) CK(cudaMemsetAsync(d_cold.p, 0, total, s));
         dd.cold = d_cold.p;
       }
       dd.queue_wait = mk(d_qw, dump->queue_wait_s);
@@ -726,10 +730,12 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
       dd.evict_cap = dump->evict_cap;
       if (dump->evict_model && dump->evict_cap > 0) {
         d_em.alloc((size_t)nd * dump->evict_cap, s);
+        CK(cudaMemsetAsync(d_em.p, 0, (size_t)nd * dump->evict_cap * sizeof(int32_t), s));
         dd.evict_model = d_em.p;
       }
       if (dump->evict_clock && dump->evict_cap > 0) {
         d_ec.alloc((size_t)nd * dump->evict_cap, s);
+        CK(cudaMemsetAsync(d_ec.p, 0, (size_t)nd * dump->evict_cap * sizeof(double), s));
         dd.evict_clock = d_ec.p;
       }
       d_nev.alloc(nd, s);

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
       }
       const uint32_t excl = incl - sum;
       const uint32_t k = s_krem[t];
+      __syncwarp();  // every lane has read s_krem[t] before one lane rewrites it
       if (k >= excl && k < incl) {  // exactly one lane holds rank k's bin
         uint32_t cum = excl;
         int d = -1;

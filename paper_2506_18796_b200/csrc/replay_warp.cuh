@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   double* p4t = wp4 + (size_t)warp * M;
   // exact p4 of every model (policy.cpp:66-67), once per scenario
   for (int m = lane; m < M; m += 32) p4t[m] = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (s_tok[m] / norm);
+  __syncwarp();  // the table is read by every lane's decisions
   const bool bitmap = need_win && w <= 1024;  // rank from the first-occurrence map
   uint32_t fo = 0;  // this lane's 32 positions of the map
 

@@ -1,5 +1,6 @@
-"""Small replay through both kernels (lane and warp, summary and dump modes)
-for compute-sanitizer runs (tools/gpu_sanitize.sh)."""
+"""Small replay through both kernels (lane and warp, summary and dump modes),
+the metrics select kernel and the policy-level kernels, for compute-sanitizer
+runs (tools/gpu_sanitize.sh)."""
 import os
 import sys
 
@@ -17,11 +18,13 @@ for catalog in (synth.eight_model_catalog(), api.ModelCatalog.synthetic_pool(80,
     for _ in range(70):
         rows.append((int(rng.integers(0, 2)),
                      PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.uniform(0, 2)),
-                                  window_length=int(rng.choice([1, 3, 10, 100])), p1_mode=int(rng.integers(0, 2))),
+                                  window_length=int(rng.choice([1, 3, 10, 100, 2000])), p1_mode=int(rng.integers(0, 2))),
                      ClusterConfig(num_accelerators=int(rng.integers(1, 17)), unload_time_s=float(rng.choice([0, 1.0])))))
     sc = api.make_scenarios(rows)
     for kern in (api.KERNEL_AUTO, api.KERNEL_WARP):
         a = P.run_batch(traces, catalog, sc, kernel=kern)
         b, _ = P.run_batch(traces, catalog, sc, kernel=kern, dump_scenarios=[0, 5, 9])
         assert (a["outcome_hash"] == b["outcome_hash"]).all()
+    m = P.run_metrics(traces, catalog, sc, raise_on_error=False)
+    assert (m["status"] == 0).all()
 print("sanitize run ok")
