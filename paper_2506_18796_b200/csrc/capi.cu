@@ -458,21 +458,21 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C, int MW, bool DUMP>
+template <int C, int MW, bool DUMP, int MINB>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DUMP>,
+    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DUMP, MINB>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
-  replay_lane_kernel<C, MW, DUMP><<<grid, LANE_BLOCK, smem, s>>>(P);
+  replay_lane_kernel<C, MW, DUMP, MINB><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 
-template <int MW, bool DUMP>
+template <int MW, bool DUMP, int MINB = CACE_LANE_MIN_BLOCKS>
 void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   switch (C) {
 #define CASE(k) \
-  case k: launch_lane<k, MW, DUMP>(P, count, smem, s); break;
+  case k: launch_lane<k, MW, DUMP, MINB>(P, count, smem, s); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
@@ -500,8 +500,12 @@ void dispatch_warp(bool dump, int spl, const ReplayParams& P, int64_t count, cud
 }
 
 void dispatch_lane(bool dump, int C, const ReplayParams& P, int64_t count, size_t smem,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool latency) {
   const bool mw1 = P.cat.M <= 32;
+  if (latency && !dump && mw1) {
+    dispatch_lane_c<1, false, kLaneLatencyMinBlocks>(C, P, count, smem, s);
+    return;
+  }
   if (dump)
     mw1 ? dispatch_lane_c<1, true>(C, P, count, smem, s) : dispatch_lane_c<2, true>(C, P, count, smem, s);
   else
@@ -533,6 +537,14 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   // than a wave), then join back onto s.
   const bool dump_on = dump.slot != nullptr;
   const size_t nseg = e->segs.size();
+  // Shallow sweeps (a few waves of lane warps) are bound by each warp's
+  // per-request dependency chain: use the register-rich instantiations.
+  int64_t lane_warps = 0;
+  for (const auto& g : e->segs)
+    if (!g.warp) lane_warps += (g.e - g.b) / 32;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+  const bool latency = lane_warps < (int64_t)5 * sms * (4 * LANE_BLOCK / 32);
   if (nseg > 0) {
     CK(cudaEventRecord(e->fork, s));
     for (size_t k = 0; k < nseg; ++k) {
@@ -544,7 +556,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
       if (g.warp)
         dispatch_warp(dump_on, g.C, P, g.e - g.b, ws);
       else
-        dispatch_lane(dump_on, g.C, P, g.e - g.b, lane_smem_bytes(M, g.C), ws);
+        dispatch_lane(dump_on, g.C, P, g.e - g.b, lane_smem_bytes(M, g.C), ws, latency);
       ++e->last_launches;
     }
     if (nseg > 1)

@@ -693,8 +693,15 @@ inline size_t lane_smem_bytes(int M, int C) {
   return a + (LANE_BLOCK / 32) * lane_smem_warp(M);
 }
 
-template <int C, int MW, bool DUMP>
-__global__ void __launch_bounds__(LANE_BLOCK, CACE_LANE_MIN_BLOCKS) replay_lane_kernel(ReplayParams P) {
+// MINB = resident blocks per SM the register allocation targets:
+// CACE_LANE_MIN_BLOCKS (4: 16 warps/SM, 128 registers) for throughput on
+// large sweeps; 3 (12 warps/SM, up to 168 registers: a shorter per-request
+// dependency chain) when the sweep is only a few waves deep and every warp's
+// chain length bounds the step (capi.cu picks).
+constexpr int kLaneLatencyMinBlocks = 3;
+
+template <int C, int MW, bool DUMP, int MINB = CACE_LANE_MIN_BLOCKS>
+__global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = P.cat.M;
   double* s_lt = reinterpret_cast<double*>(smem);
