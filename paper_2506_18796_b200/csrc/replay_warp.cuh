@@ -157,16 +157,19 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   double na = 0.0, npf = 0.0, ndc = 0.0;
   uint32_t nnxt = 0, nmc = 0;
   if (n > 0) load_rec(tr, na, npf, ndc, nnxt, nmc);
+  uint32_t eprv_next = (bitmap && 1024 < n) ? __ldg(&tr[1024].prv) : 0u;
   for (uint32_t k = 0; k < n; ++k) {
     const double a = na, pf = npf, dc = ndc;
     const uint32_t nxt = nnxt, mc = nmc;
     if (k + 1 < n) load_rec(tr + k + 1, na, npf, ndc, nnxt, nmc);
-    // window maintenance inputs, needed only at the end of the iteration
+    // window maintenance inputs, needed only at the end of the iteration;
+    // the entering position's prv (1024 requests ahead: an L2/DRAM load) is
+    // fetched one iteration early
     double nxa = 0.0;
-    uint32_t eprv = 0u;
+    const uint32_t eprv = eprv_next;
     if (need_win) {
       nxa = __ldg(&tr[k].nxa);
-      if (bitmap && k + 1024 < n) eprv = __ldg(&tr[k + 1024].prv);
+      if (bitmap && k + 1025 < n) eprv_next = __ldg(&tr[k + 1025].prv);
     }
     const int m = (int)(mc & 0xffffu);
 
@@ -317,7 +320,10 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
             }
             const double p2 = variant == CACE_MINUS_P2 ? 0.0 : s_p2[ms];
             double p3 = 0.0;
-            if (variant != CACE_MINUS_P3) p3 = wrk[j] >= 0 ? (double)wrk[j] / wd : 1.0;
+            if (variant != CACE_MINUS_P3) {
+              p3 = 1.0;
+              if (wrk[j] >= 0) p3 = (double)wrk[j] / wd;
+            }
             const double p4 = p4t[ms];
             const double T = ((p1 + p2) + p3) + p4;
             tnan[j] = T != T;
