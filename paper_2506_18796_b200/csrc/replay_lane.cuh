@@ -738,7 +738,9 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
   const int variant = P.scen[sidx].variant;
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
-  const bool warp_win = __any_sync(kFull, need_win);
+  // With capacity >= pool size every model fits: no eviction decision ever
+  // happens, so the lookahead window is never read and is not maintained.
+  const bool warp_win = __any_sync(kFull, need_win) && C < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x,
                    l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
