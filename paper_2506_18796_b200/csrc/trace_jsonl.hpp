@@ -13,7 +13,8 @@
 //     arrival, non-positive token counts, arrivals out of order;
 //   * the FIRST failing line (in file order) is reported with the
 //     reference's message text.  Field errors reproduce nlohmann's
-//     out_of_range.403 / type_error.302 texts; JSON syntax errors keep the
+//     out_of_range.403 / type_error.302 texts (and out_of_range.406 for
+//     overflowing numbers); JSON syntax errors keep the
 //     reference's "trace line N: invalid JSON: " prefix with this parser's own
 //     description (nlohmann's parse_error wording is not reproduced).
 // Numbers: integers parse exactly (uint64 / int64, larger ones as double),
@@ -209,6 +210,8 @@ struct Parser {
     }
     v.kind = K_DOUBLE;
     v.d = std::strtod(tok.c_str(), nullptr);
+    if (!std::isfinite(v.d))  // nlohmann rejects overflowing literals (lexer, out_of_range.406)
+      throw LineError{"[json.exception.out_of_range.406] number overflow parsing '" + tok + "'"};
   }
   void skip_value(int depth) {
     if (depth > 512) fail("nesting too deep");

@@ -130,6 +130,13 @@ def test_syntax_errors_same_prefix(ref, text):
     _err(ref, text, prefix_only=True)
 
 
+def test_number_overflow_matches_reference_text(ref):
+    """Overflowing literals are a parse error in nlohmann (out_of_range.406);
+    found by the fuzz test — the full message matches."""
+    _err(ref, HDR + _rec(0, 1.0).replace(b'"arrival_time_s": 1.0', b'"arrival_time_s": 4.2e999'))
+    _err(ref, HDR.replace(b'"rate":2.5', b'"rate":-1e400'))
+
+
 def test_out_of_order_across_chunks(ref):
     """The arrival-order check spans the per-thread chunk boundaries."""
     lines = [HDR]
@@ -151,3 +158,58 @@ def test_load_trace_file(ref, tmp_path):
     with pytest.raises(api.SimError) as e:
         api.load_trace(str(tmp_path / "missing.jsonl"), api.ModelCatalog.build_default())
     assert str(e.value) == "trace: cannot open: " + str(tmp_path / "missing.jsonl")
+
+
+def test_fuzz_against_reference(ref):
+    """Randomly mutated traces (dropped / duplicated / retyped fields, junk
+    bytes, reordered lines, extra keys): the parsed trace or the error text
+    equals the reference parser's (syntax errors: same prefix)."""
+    rng = np.random.default_rng(77)
+    base = ref.serialize_built_trace(2, 8.0, 20.0, 9, 1).split(b"\n")
+    mutations = 0
+    for case in range(300):
+        lines = list(base)
+        for _ in range(int(rng.integers(1, 4))):
+            i = int(rng.integers(0, len(lines)))
+            op = int(rng.integers(0, 9))
+            ln = lines[i]
+            if op == 0:
+                lines[i] = ln.replace(b'"prompt_tokens"', b'"prompt_token"', 1)
+            elif op == 1:
+                lines[i] = ln.replace(b'"python"', b'"cobol"', 1)
+            elif op == 2 and len(ln) > 3:
+                j = int(rng.integers(1, len(ln)))
+                lines[i] = ln[:j] + bytes([int(rng.integers(32, 127))]) + ln[j + 1:]
+            elif op == 3 and len(ln) > 3:
+                lines[i] = ln[: int(rng.integers(1, len(ln)))]
+            elif op == 4 and i + 1 < len(lines):
+                lines[i], lines[i + 1] = lines[i + 1], lines[i]
+            elif op == 5:
+                lines[i] = ln.replace(b"}", b',"extra":{"a":[1,2.5e3,"x"]}}', 1)
+            elif op == 6:
+                lines[i] = ln.replace(b'"output_tokens":', b'"output_tokens":"', 1)
+            elif op == 7:
+                lines.insert(i, b"")
+            else:
+                lines[i] = ln.replace(b'"arrival_time_s":', b'"arrival_time_s":-', 1)
+            mutations += 1
+        text = b"\n".join(lines)
+        try:
+            want = ref.parse_trace(text)
+            err = None
+        except Exception as e:  # noqa: BLE001
+            want, err = None, str(e)
+        if err is None:
+            tr, hdr, rid = _ours(text)
+            assert np.array_equal(tr.arrival_time_s.view(np.uint64), want["arrival"].view(np.uint64)), case
+            assert np.array_equal(rid, want["request_id"]) and np.array_equal(tr.output_tokens, want["output"]), case
+        else:
+            with pytest.raises(api.SimError) as e_ours:
+                _ours(text)
+            got = str(e_ours.value)
+            if "invalid JSON: " in err:
+                k = err.index("invalid JSON: ") + len("invalid JSON: ")
+                assert got[:k] == err[:k], (case, err, got)
+            else:
+                assert got == err, (case, err, got)
+    assert mutations > 300
