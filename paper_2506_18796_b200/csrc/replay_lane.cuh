@@ -314,6 +314,7 @@ struct LaneSmem {
   float* p4f;        // [M] p2 + p4 = p2 + w1 * (tokens / normalizer), fp32 (screening)
   double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67)
   double* done;      // [C] |stime|: completion time of the slot's last service
+  float* prm;        // [4] screen constants: 1/w, p1 scale, p1 offset, margin (+inf: no screen)
   uint32_t* seq;     // [C] ServiceComplete push seq of each busy slot
   int* word;         // [C] slot word: model | lex rank << 18
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
@@ -338,10 +339,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const bool verbatim = sc.p1_mode == CACE_P1_VERBATIM;
   const uint32_t w = (uint32_t)sc.window_length;
   const double norm = (double)sc.output_token_normalizer;
-  const float rcpw = 1.0f / (float)sc.window_length;
+
   // fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0
-  const float p1s = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
-  const float p1o = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
+
   const int st = S.stride;
   // fp32 screening is valid while every p2 + p4 is finite and moderate; the
   // event clock is finite (validated on the host) and t < 1e30 below.
@@ -362,7 +362,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (screen_ok) tbound = fmaxf(tbound, 2.0f + fabsf((float)(p2 + p4)));
     }
   }
-  const float margin = 6e-5f + 1e-6f * (tbound + 4.0f);
+  // screen constants live in shared memory: read only by deciding lanes, so
+  // they hold no registers across the replay loop
+  S.prm[0] = 1.0f / (float)sc.window_length;
+  S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);  // p1 = p1s * p1v + p1o
+  S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
+  S.prm[3 * st] = screen_ok ? 6e-5f + 1e-6f * (tbound + 4.0f) : INFINITY;
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -399,7 +404,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   uint64_t ho = CACE_HASH_SEED;
   double lo_sum = 0.0;
   uint64_t he = CACE_HASH_SEED;
-  const double unload = sc.unload_time_s;
 
   for (uint32_t c = 0, k = 0; k < n; ++c) {
   const ReqRec* const cb = rs.chunk(c);
@@ -513,6 +517,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             // approximate reciprocal, rank*(1/w), p4 = w1*tok*(1/norm), the
             // term conversions and three fp32 sums add <= 2^-21 (|T| + 4).
             // The margin is twice the worst case.
+            const float rcpw = S.prm[0], p1s = S.prm[st], p1o = S.prm[2 * st];
             float best = -INFINITY, second = -INFINITY;
             int bs = 0;
             const uint32_t wend = k + w;
@@ -534,7 +539,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               best = fmaxf(best, T);
             }
             v = bs;
-            if (!screen_ok || !(best - second > margin)) {
+            if (!(best - second > S.prm[3 * st])) {
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
               // strict max in (last_used, model_id) order"
               // (policy.cpp:92-113), bit-identical to the reference; taken on
@@ -587,7 +592,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           }
           ++dn_ev;
         }
-        ud = unload;
+        ud = __ldg(&P.scen[sidx].unload_time_s);
       }
       // start_load (engine.cpp:123-132), then blocked until LoadComplete
       // (r, 0, .): completions strictly before r idle their slots.
@@ -685,7 +690,7 @@ constexpr int LANE_BLOCK = 128;
 // window table.
 inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
 inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
-  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + C * 8 + M);
+  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + 4 * 4 + C * 8 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M) { return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt); }
 inline size_t lane_smem_bytes(int M, int C) {
@@ -714,7 +719,8 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   double* l_p4d = reinterpret_cast<double*>(smem + ((lane_smem_cat(M) + 7) & ~(size_t)7));  // [M][LB]
   double* l_done = l_p4d + (size_t)M * LANE_BLOCK;                                          // [C][LB]
   float* l_p4f = reinterpret_cast<float*>(l_done + (size_t)C * LANE_BLOCK);                // [M][LB]
-  uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_p4f + (size_t)M * LANE_BLOCK);  // [C][LANE_BLOCK]
+  float* l_prm = l_p4f + (size_t)M * LANE_BLOCK;                                  // [4][LANE_BLOCK]
+  uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_prm + (size_t)4 * LANE_BLOCK);  // [C][LANE_BLOCK]
   int* l_word = reinterpret_cast<int*>(l_seq + (size_t)C * LANE_BLOCK);          // [C][LANE_BLOCK]
   uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_word + (size_t)C * LANE_BLOCK);  // [M][LANE_BLOCK]
   unsigned char* wbase =
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   // happens, so the lookahead window is never read and is not maintained.
   const bool warp_win = __any_sync(kFull, need_win) && C < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
-  const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x,
+  const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x, l_prm + threadIdx.x,
                    l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win};
   replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);

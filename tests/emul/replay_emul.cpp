@@ -46,12 +46,12 @@ template <int C, bool D>
 static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
-  std::vector<float> p4f(P.cat.M);
+  std::vector<float> p4f(P.cat.M), prm(4);
   std::vector<double> p4d(P.cat.M), done(C);
   std::vector<uint32_t> seq(C);
   std::vector<int> word(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), p4d.data(), done.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr};
+  const LaneSmem S{p4f.data(), p4d.data(), done.data(), prm.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr};
   replay_scenario<C, 2, D>(P, i, false, need_win, K, S);
 }
 
