@@ -325,7 +325,11 @@ struct LaneSmem {
 
 // Replays one scenario (see the file comment).  shadow lanes (warp padding)
 // replay a copy of a real scenario for lockstep and write nothing.
-template <int C, int MW, bool DUMP>
+// XR: the exact fallback as rolled loops over the idle slots reading the
+// shared-memory shadows (fewer live registers: best for the 16-warp
+// instantiations) or unrolled over the slot registers (best when registers
+// are plentiful, the 12-warp instantiations).
+template <int C, int MW, bool DUMP, bool XR = true>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
                                 const CatShared& K, const LaneSmem& S) {
   const cace_scenario_t sc = P.scen[sidx];
@@ -547,6 +551,58 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               // One pass: the best non-NaN total, ties to the earlier entry in
               // (last_used, lex) order; a NaN sorted-first entry keeps the
               // slot (no later total compares greater than NaN).
+              if constexpr (XR) {
+              // Rolled loops over the idle slots, reading last_used from the
+              // shared completion-time shadow (equal to |stime| once Idle):
+              // compact code and few live registers for this rare path.
+              unsigned idm = 0;
+#pragma unroll
+              for (int s = 0; s < C; ++s) idm |= is_idle(stime[s]) ? (1u << s) : 0u;
+              int f = -1;
+              double flu = 0.0;
+              int flex = 0;
+#pragma unroll 1
+              for (unsigned q = idm; q; q &= q - 1u) {  // sorted-first: min (last_used, lex)
+                const int s = __ffs(q) - 1;
+                const double lu = S.done[s * st];
+                const int lx = slot_lex(S.word[s * st]);
+                if (f < 0 || lu < flu || (lu == flu && lx < flex)) {
+                  f = s;
+                  flu = lu;
+                  flex = lx;
+                }
+              }
+              bool f_nan = false;
+              double bt = 0.0, blu = 0.0;
+              int blex = 0, bv = -1;
+#pragma unroll 1
+              for (unsigned q = idm; q; q &= q - 1u) {
+                const int s = __ffs(q) - 1;
+                const double lu = S.done[s * st];
+                const int wd = S.word[s * st];
+                const int ms = slot_model(wd);
+                const int lx = slot_lex(wd);
+                const double p1 = variant == CACE_MINUS_P1
+                                      ? 0.0
+                                      : exact_p1(now, lu, verbatim, P.log_variant, P.log_tab, P.log_tab2);
+                const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
+                double p3 = 0.0;
+                if (variant != CACE_MINUS_P3) {
+                  const WinEnt e = win.gather(ms);
+                  p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
+                }
+                const double p4 = S.p4d[ms * st];
+                const double T = ((p1 + p2) + p3) + p4;
+                if (s == f) f_nan = T != T;
+                if (T == T && (bv < 0 || T > bt || (T == bt && (lu < blu || (lu == blu && lx < blex))))) {
+                  bt = T;
+                  blu = lu;
+                  blex = lx;
+                  bv = s;
+                }
+              }
+              v = f_nan ? f : bv;
+              } else {
               const int f = sorted_first();
               bool f_nan = false;
               double bt = 0.0, blu = 0.0;
@@ -578,6 +634,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 }
               }
               v = f_nan ? f : bv;
+              }
             }
           }
         }
@@ -751,7 +808,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x, l_prm + threadIdx.x,
                    l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win};
-  replay_scenario<C, MW, DUMP>(P, sidx, shadow, warp_win, K, S);
+  replay_scenario<C, MW, DUMP, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
 }
 #endif  // CACE_HOST_EMULATION
 

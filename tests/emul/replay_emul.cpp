@@ -42,6 +42,8 @@ using namespace cace;
 static const double kTab[256] = CACE_GLIBC_LOG_TAB;
 static const double kTab2[256] = CACE_GLIBC_LOG_TAB2;
 
+static int g_xr = 1;  // exact fallback variant: 1 rolled (16-warp kernels), 0 unrolled (12-warp)
+
 template <int C, bool D>
 static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
@@ -52,7 +54,10 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   std::vector<int> word(C);
   std::vector<uint8_t> slot_of(P.cat.M);
   const LaneSmem S{p4f.data(), p4d.data(), done.data(), prm.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr};
-  replay_scenario<C, 2, D>(P, i, false, need_win, K, S);
+  if (g_xr)
+    replay_scenario<C, 2, D, true>(P, i, false, need_win, K, S);
+  else
+    replay_scenario<C, 2, D, false>(P, i, false, need_win, K, S);
 }
 
 extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -61,7 +66,8 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
                                      const int32_t* dump_slot, const int64_t* dump_off,
                                      uint8_t* cold, double* ttft, double* e2e, double* qw, double* lw,
                                      int64_t evict_cap, int32_t* evict_model, double* evict_clock,
-                                     int64_t* n_evict) {
+                                     int64_t* n_evict, int32_t xr) {
+  g_xr = xr;
   try {
     HostCatalog cat;
     cat.load(catalog);

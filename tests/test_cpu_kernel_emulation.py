@@ -26,8 +26,8 @@ def _logv():
     return api.probe_log_variant()
 
 
-def _check_full(ref, emul, catalog, traces, sc):
-    got, d = emul.replay_batch(traces, catalog, sc, _logv(), dump=True)
+def _check_full(ref, emul, catalog, traces, sc, rolled_exact=True):
+    got, d = emul.replay_batch(traces, catalog, sc, _logv(), dump=True, rolled_exact=rolled_exact)
     rcat = ref_catalog(ref, catalog)
     for k in range(len(sc)):
         want = ref.run(rcat, ref_trace(traces[int(sc[k]["trace"])]), ref_scenario(ref, sc[k]))
@@ -50,8 +50,9 @@ def _check_full(ref, emul, catalog, traces, sc):
         assert np.array_equal(bits(d["ec"][k * cap:k * cap + ne]), bits(want.evict_clock)), f"{ctx} clocks"
 
 
+@pytest.mark.parametrize("rolled", [True, False], ids=["rolled_exact", "unrolled_exact"])
 @pytest.mark.parametrize("seed", range(8))
-def test_emulated_kernel_random_scenarios(ref, emul, seed):
+def test_emulated_kernel_random_scenarios(ref, emul, seed, rolled):
     from paper_2506_18796_b200 import api, synth
     from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig
 
@@ -68,7 +69,7 @@ def test_emulated_kernel_random_scenarios(ref, emul, seed):
         cl = ClusterConfig(num_accelerators=int(rng.integers(1, 11)),
                            unload_time_s=float(rng.choice([0.0, 0.0, 0.5, 2.0])))
         rows.append((int(rng.integers(0, 3)), pol, cl))
-    _check_full(ref, emul, catalog, traces, api.make_scenarios(rows))
+    _check_full(ref, emul, catalog, traces, api.make_scenarios(rows), rolled_exact=rolled)
 
 
 def test_emulated_kernel_ties_and_unsorted(ref, emul):
