@@ -537,14 +537,18 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   // than a wave), then join back onto s.
   const bool dump_on = dump.slot != nullptr;
   const size_t nseg = e->segs.size();
-  // Shallow sweeps (< 10 waves of lane warps) are bound by each warp's
+  // Shallow sweeps (< 5 waves of lane warps) are bound by each warp's
   // per-request dependency chain: use the register-rich instantiations.
   int64_t lane_warps = 0;
   for (const auto& g : e->segs)
     if (!g.warp) lane_warps += (g.e - g.b) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
-  const bool latency = lane_warps < (int64_t)10 * sms * (4 * LANE_BLOCK / 32);
+  static const int waves = [] {
+    const char* v = std::getenv("CACE_LATENCY_WAVES");  // tuning override
+    return v ? std::atoi(v) : 5;
+  }();
+  const bool latency = lane_warps < (int64_t)waves * sms * (4 * LANE_BLOCK / 32);
   if (nseg > 0) {
     CK(cudaEventRecord(e->fork, s));
     for (size_t k = 0; k < nseg; ++k) {
