@@ -216,10 +216,11 @@ struct Window {
   }
   // Per lane (no collective): model ms's entry.
   __device__ __forceinline__ WinEnt gather(int ms) const { return tab[ms]; }
-  // Collective, split so the ballot/popc latency overlaps the request's own
-  // dependency chain: prepare (top of the iteration) computes the state after
-  // the head (model mk) is served -- mk's first becomes nx -- without
-  // touching what this iteration's decisions read; commit (end) installs it.
+  // Collective: prepare computes the state after the head (model mk) is
+  // served -- mk's first becomes nx -- without touching what the iteration's
+  // decisions read; commit installs it.  (Issuing prepare at the top of the
+  // iteration to overlap the ballot latency measured slower; the replay loop
+  // calls them back to back at the end.)
   uint32_t nf[MW], nr[MW];
   int pmk;
   __device__ __forceinline__ void prepare(int mk, uint32_t nx) {
