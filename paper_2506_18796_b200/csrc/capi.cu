@@ -250,6 +250,7 @@ struct cace_engine {
     bool warp;  // warp-per-scenario kernel
   };
   std::vector<Seg> segs;
+  std::vector<int64_t> h_order;  // plan entries (scenario index | kShadowBit)
   DBuf<int64_t> d_order;
   std::vector<int64_t> bad_idx;
   std::vector<int32_t> bad_code;
@@ -455,6 +456,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
   e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);
   CK(cudaStreamSynchronize(e->stream));
+  e->h_order = std::move(order);
   e->plan_n = n;
 }
 
@@ -512,10 +514,8 @@ void dispatch_lane(bool dump, int C, const ReplayParams& P, int64_t count, size_
     mw1 ? dispatch_lane_c<1, false>(C, P, count, smem, s) : dispatch_lane_c<2, false>(C, P, count, smem, s);
 }
 
-void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary_t* d_out,
-            const DumpDev& dump, cudaStream_t s) {
-  if (n != e->plan_n) throw Invalid{CACE_E_INVALID, "cace: replay does not match the plan"};
-  CK(cudaSetDevice(e->device));
+ReplayParams replay_params(const cace_engine* e, const cace_scenario_t* d_sc, cace_summary_t* d_out,
+                           const DumpDev& dump) {
   ReplayParams P{};
   P.rec = e->d_rec.p;
   P.trace_off = e->d_off.p;
@@ -530,12 +530,51 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   P.order = e->d_order.p;
   P.out = d_out;
   P.dump = dump;
-  const int M = e->cat.M;
+  return P;
+}
+
+// One launch over plan entries [b, e) of segment g (b warp-aligned).
+void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams P, int64_t b,
+                  int64_t end, cudaStream_t ws, bool latency) {
+  P.seg_begin = b;
+  P.seg_end = end;
+  const bool dump_on = P.dump.slot != nullptr;
+  if (g.warp)
+    dispatch_warp(dump_on, g.C, P, end - b, ws);
+  else
+    dispatch_lane(dump_on, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C), ws, latency);
+}
+
+void fill_status(cace_engine* e, cace_summary_t* d_out, cudaStream_t s) {
+  if (e->bad_idx.empty()) return;
+  fill_status_kernel<<<(unsigned)((e->bad_idx.size() + 255) / 256), 256, 0, s>>>(
+      e->d_bad_idx.p, e->d_bad_code.p, (int64_t)e->bad_idx.size(), d_out);
+  CK(cudaGetLastError());
+  ++e->last_launches;
+}
+
+void fork_workers(cace_engine* e, cudaStream_t s, size_t used) {
+  CK(cudaEventRecord(e->fork, s));
+  for (size_t k = 0; k < std::min(used, e->workers.size()); ++k)
+    CK(cudaStreamWaitEvent(e->workers[k], e->fork, 0));
+}
+
+void join_workers(cace_engine* e, cudaStream_t s, size_t used) {
+  for (size_t k = 0; k < std::min(used, e->workers.size()); ++k) {
+    CK(cudaEventRecord(e->joins[k], e->workers[k]));
+    CK(cudaStreamWaitEvent(s, e->joins[k], 0));
+  }
+}
+
+void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary_t* d_out,
+            const DumpDev& dump, cudaStream_t s) {
+  if (n != e->plan_n) throw Invalid{CACE_E_INVALID, "cace: replay does not match the plan"};
+  CK(cudaSetDevice(e->device));
+  const ReplayParams P = replay_params(e, d_sc, d_out, dump);
   e->last_launches = 0;
   // Capacity segments are independent kernels: fork them over the engine's
   // worker streams so they share the SMs (one segment alone is often less
   // than a wave), then join back onto s.
-  const bool dump_on = dump.slot != nullptr;
   const size_t nseg = e->segs.size();
   // Shallow sweeps (< 5 waves of lane warps) are bound by each warp's
   // per-request dependency chain: use the register-rich instantiations.
@@ -550,31 +589,16 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   }();
   const bool latency = lane_warps < (int64_t)waves * sms * (4 * LANE_BLOCK / 32);
   if (nseg > 0) {
-    CK(cudaEventRecord(e->fork, s));
+    if (nseg > 1) fork_workers(e, s, nseg);
     for (size_t k = 0; k < nseg; ++k) {
       cudaStream_t ws = nseg == 1 ? s : e->workers[k % e->workers.size()];
-      if (ws != s) CK(cudaStreamWaitEvent(ws, e->fork, 0));
       const auto& g = e->segs[k];
-      P.seg_begin = g.b;
-      P.seg_end = g.e;
-      if (g.warp)
-        dispatch_warp(dump_on, g.C, P, g.e - g.b, ws);
-      else
-        dispatch_lane(dump_on, g.C, P, g.e - g.b, lane_smem_bytes(M, g.C), ws, latency);
+      launch_piece(e, g, P, g.b, g.e, ws, latency);
       ++e->last_launches;
     }
-    if (nseg > 1)
-      for (size_t k = 0; k < std::min(nseg, e->workers.size()); ++k) {
-        CK(cudaEventRecord(e->joins[k], e->workers[k]));
-        CK(cudaStreamWaitEvent(s, e->joins[k], 0));
-      }
+    if (nseg > 1) join_workers(e, s, nseg);
   }
-  if (!e->bad_idx.empty()) {
-    fill_status_kernel<<<(unsigned)((e->bad_idx.size() + 255) / 256), 256, 0, s>>>(
-        e->d_bad_idx.p, e->d_bad_code.p, (int64_t)e->bad_idx.size(), d_out);
-    CK(cudaGetLastError());
-    ++e->last_launches;
-  }
+  fill_status(e, d_out, s);
 }
 
 template <typename F>
@@ -817,103 +841,171 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
                                cace_summary_t* summaries, const cace_opts_t* opts, char* msg,
                                size_t msg_cap) {
   cace_engine* e = nullptr;
+  PhaseTimer pt;
   int32_t rc = cace_engine_create(catalog, traces, n_traces, opts, &e, msg, msg_cap);
   if (rc != CACE_OK) return rc;
+  pt.mark("engine_create");
   rc = guarded(msg, msg_cap, [&]() -> int32_t {
     if (n_scenarios > 0 && (!metrics || !scenarios))
       throw Invalid{CACE_E_INVALID, "cace: metrics / scenarios is NULL"};
     cudaStream_t s = e->stream;
-    std::vector<cace_summary_t> summ(n_scenarios);
-    // sample budget per batch: ~60% of free device memory
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = std::max<size_t>((size_t)(0.6 * (double)free_b), (size_t)64 << 20);
+    plan(e, scenarios, n_scenarios);
+    pt.mark("plan");
     auto nreq = [&](int64_t i) -> int64_t {
       const int t = scenarios[i].trace;
       return (t >= 0 && t < e->lay.T) ? e->lay.off[t + 1] - e->lay.off[t] : 0;
     };
-    std::vector<double> stat;
-    for (int64_t b0 = 0; b0 < n_scenarios;) {
-      int64_t b1 = b0;
-      size_t bytes = 0;
-      while (b1 < n_scenarios && (b1 == b0 || bytes + (size_t)nreq(b1) * 8 <= budget)) bytes += (size_t)nreq(b1++) * 8;
-      const int64_t B = b1 - b0;
-      const cace_scenario_t* sc = scenarios + b0;
-      plan(e, sc, B);
-      std::vector<int32_t> slot(B);
-      std::vector<int64_t> off(B + 1, 0);
-      std::vector<uint32_t> nc(B), nr(B);
-      for (int64_t i = 0; i < B; ++i) {
-        slot[i] = (int32_t)i;
-        const int t = sc[i].trace;
-        const bool tv = t >= 0 && t < e->lay.T;
-        nr[i] = (uint32_t)nreq(b0 + i);
-        nc[i] = tv ? e->lay.ncomp[t] : 0;
-        off[i + 1] = off[i] + nr[i];
+    // Pipeline: the planned sweep (heaviest segments first) is cut into
+    // warp-aligned chunks whose samples fit one of W ring buffers (~60% of
+    // free HBM in total); chunk j replays into buffer j % W on worker stream
+    // j % W and the select kernel reduces it on the same stream, so the
+    // buffer is reused in stream order while the other streams keep the SMs
+    // full of replay lanes.  Chunk-local arrays are concatenated in chunk
+    // order (position p = chunk base + local index).
+    const size_t W = e->workers.size();
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    // memory the stream-ordered pool holds but does not use is free to us
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, e->device) == cudaSuccess) {
+      uint64_t reserved = 0, used = 0;
+      if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+        free_b += reserved - used;
+    }
+    cudaGetLastError();
+    size_t budget = std::max<size_t>((size_t)(0.6 * (double)free_b), (size_t)64 << 20);
+    if (const char* v = std::getenv("CACE_METRICS_BUDGET_MB"))  // test / tuning override
+      budget = std::max<size_t>((size_t)std::atoll(v) << 20, 1);
+    const size_t per = budget / W;
+    struct Chunk {
+      size_t seg;
+      int64_t b, e, base, nloc, nsamp;
+    };
+    std::vector<Chunk> chunks;
+    std::vector<int32_t> slot(n_scenarios, -1);
+    std::vector<int64_t> loc_scen, off;
+    std::vector<uint32_t> nc, nr;
+    const auto& order = e->h_order;
+    for (size_t k = 0; k < e->segs.size(); ++k) {
+      const auto& g = e->segs[k];
+      for (int64_t pos = g.b; pos < g.e;) {
+        Chunk c{k, pos, pos, (int64_t)loc_scen.size(), 0, 0};
+        while (c.e < g.e) {
+          const int64_t ue = std::min<int64_t>(c.e + 32, g.e);
+          int64_t ub = 0;
+          for (int64_t q = c.e; q < ue; ++q)
+            if (!(order[q] & (int64_t)kShadowBit)) ub += nreq(order[q]);
+          if (c.e > c.b && (size_t)(c.nsamp + ub) * 8 > per) break;
+          for (int64_t q = c.e; q < ue; ++q) {
+            if (order[q] & (int64_t)kShadowBit) continue;
+            const int64_t si = order[q];
+            const int t = scenarios[si].trace;
+            slot[si] = (int32_t)(loc_scen.size() - c.base);
+            loc_scen.push_back(si);
+            off.push_back(c.nsamp);
+            nr.push_back((uint32_t)nreq(si));
+            nc.push_back(e->lay.ncomp[t]);
+            c.nsamp += nreq(si);
+          }
+          c.e = ue;
+        }
+        c.nloc = (int64_t)loc_scen.size() - c.base;
+        chunks.push_back(c);
+        pos = c.e;
       }
-      DBuf<cace_scenario_t> d_sc;
-      d_sc.upload(sc, B, s);
-      DBuf<cace_summary_t> d_out;
-      d_out.alloc(B, s);
-      DBuf<int32_t> d_slot;
-      DBuf<int64_t> d_off;
-      DBuf<uint32_t> d_nc, d_nr;
-      DBuf<double> d_samp, d_stat;
-      d_slot.upload(slot.data(), B, s);
-      d_off.upload(off.data(), B + 1, s);
-      d_nc.upload(nc.data(), B, s);
-      d_nr.upload(nr.data(), B, s);
-      d_samp.alloc(std::max<int64_t>(off[B], 1), s);
-      d_stat.alloc((size_t)B * 8, s);
-      DumpDev dd{};
-      dd.slot = d_slot.p;
-      dd.dump_off = d_off.p;
-      dd.samples = d_samp.p;
-      replay(e, d_sc.p, B, d_out.p, dd, s);
-      MetricsParams mp{d_samp.p, d_off.p, d_nc.p, d_nr.p, d_stat.p};
-      if (B > 0) metrics_select_kernel<<<(unsigned)(2 * B), METRICS_BLOCK, 0, s>>>(mp);
-      CK(cudaGetLastError());
-      stat.resize((size_t)B * 8);
-      CK(cudaMemcpyAsync(summ.data() + b0, d_out.p, B * sizeof(cace_summary_t), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(stat.data(), d_stat.p, (size_t)B * 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      // RunMetrics (compute_run_metrics, metrics.cpp:35-62)
-      for (int64_t i = 0; i < B; ++i) {
-        const cace_summary_t& o = summ[b0 + i];
-        cace_run_metrics_t& m = metrics[b0 + i];
-        std::memset(&m, 0, sizeof(m));
-        m.status = o.status;
-        if (o.status != CACE_OK) continue;
-        if (o.hits + o.misses == 0) {
-          m.status = CACE_E_METRICS_EMPTY;
-          continue;
-        }
-        if (nc[i] == 0) {
-          m.status = CACE_E_METRICS_NO_TTFT;
-          continue;
-        }
-        if (nr[i] - nc[i] == 0) {
-          m.status = CACE_E_METRICS_NO_E2E;
-          continue;
-        }
-        m.cache_hit_rate = (double)o.hits / (double)(o.hits + o.misses);
-        m.load_overhead_s = o.load_overhead_s;
-        m.evictions = (double)o.evictions;
-        const double* st = stat.data() + (size_t)i * 8;
-        auto fill = [&](cace_latency_summary_t& ls, uint64_t cnt, double sum, const double* q) {
-          ls.count = cnt;
-          ls.mean_s = sum / (double)cnt;  // replay-order sum (the reference sums the sorted samples)
-          ls.p50_s = q[0];
-          ls.p95_s = q[1];
-          ls.p99_s = q[2];
-          ls.max_s = q[3];
-        };
-        fill(m.ttft_completion, nc[i], o.sum_ttft_completion, st);
-        fill(m.e2e_reasoning, nr[i] - nc[i], o.sum_e2e_reasoning, st + 4);
+    }
+    const int64_t NL = (int64_t)loc_scen.size();
+    pt.mark("chunks");
+    std::vector<int64_t> ring_len(W, 0);
+    for (size_t j = 0; j < chunks.size(); ++j)
+      ring_len[j % W] = std::max(ring_len[j % W], chunks[j].nsamp);
+    DBuf<cace_scenario_t> d_sc;
+    d_sc.upload(scenarios, n_scenarios, s);
+    DBuf<cace_summary_t> d_out;
+    d_out.alloc(n_scenarios, s);
+    DBuf<int32_t> d_slot;
+    DBuf<int64_t> d_off;
+    DBuf<uint32_t> d_nc, d_nr;
+    DBuf<double> d_stat;
+    d_slot.upload(slot.data(), n_scenarios, s);
+    d_off.upload(off.data(), NL, s);
+    d_nc.upload(nc.data(), NL, s);
+    d_nr.upload(nr.data(), NL, s);
+    d_stat.alloc((size_t)std::max<int64_t>(NL, 1) * 8, s);
+    std::vector<DBuf<double>> ring(W);
+    for (size_t r = 0; r < W; ++r)
+      if (ring_len[r] > 0) ring[r].alloc(ring_len[r], s);
+    DumpDev dd{};
+    dd.slot = d_slot.p;
+    const ReplayParams P0 = replay_params(e, d_sc.p, d_out.p, dd);
+    e->last_launches = 0;
+    fork_workers(e, s, chunks.size());
+    for (size_t j = 0; j < chunks.size(); ++j) {
+      const Chunk& c = chunks[j];
+      cudaStream_t ws = e->workers[j % W];
+      ReplayParams P = P0;
+      P.dump.dump_off = d_off.p + c.base;
+      P.dump.samples = ring[j % W].p;
+      launch_piece(e, e->segs[c.seg], P, c.b, c.e, ws, false);
+      ++e->last_launches;
+      if (c.nloc > 0) {
+        MetricsParams mp{ring[j % W].p, d_off.p + c.base, d_nc.p + c.base, d_nr.p + c.base,
+                         d_stat.p + (size_t)c.base * 8};
+        metrics_select_kernel<<<(unsigned)(2 * c.nloc), METRICS_BLOCK, 0, ws>>>(mp);
+        CK(cudaGetLastError());
+        ++e->last_launches;
       }
-      b0 = b1;
+    }
+    join_workers(e, s, chunks.size());
+    fill_status(e, d_out.p, s);
+    std::vector<cace_summary_t> summ(n_scenarios);
+    std::vector<double> stat((size_t)NL * 8);
+    if (n_scenarios > 0)
+      CK(cudaMemcpyAsync(summ.data(), d_out.p, n_scenarios * sizeof(cace_summary_t), cudaMemcpyDeviceToHost, s));
+    if (NL > 0) CK(cudaMemcpyAsync(stat.data(), d_stat.p, (size_t)NL * 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    pt.mark("replay+select");
+    for (auto& r : ring) r.release();
+    // RunMetrics (compute_run_metrics, metrics.cpp:35-62)
+    std::vector<int64_t> pos(n_scenarios, -1);
+    for (int64_t p = 0; p < NL; ++p) pos[loc_scen[p]] = p;
+    for (int64_t i = 0; i < n_scenarios; ++i) {
+      const cace_summary_t& o = summ[i];
+      cace_run_metrics_t& m = metrics[i];
+      std::memset(&m, 0, sizeof(m));
+      m.status = o.status;
+      if (o.status != CACE_OK) continue;
+      const int64_t p = pos[i];
+      if (p < 0 || o.hits + o.misses == 0) {  // p < 0: a valid scenario on an empty trace
+        m.status = CACE_E_METRICS_EMPTY;
+        continue;
+      }
+      if (nc[p] == 0) {
+        m.status = CACE_E_METRICS_NO_TTFT;
+        continue;
+      }
+      if (nr[p] - nc[p] == 0) {
+        m.status = CACE_E_METRICS_NO_E2E;
+        continue;
+      }
+      m.cache_hit_rate = (double)o.hits / (double)(o.hits + o.misses);
+      m.load_overhead_s = o.load_overhead_s;
+      m.evictions = (double)o.evictions;
+      const double* st = stat.data() + (size_t)p * 8;
+      auto fill = [&](cace_latency_summary_t& ls, uint64_t cnt, double sum, const double* q) {
+        ls.count = cnt;
+        ls.mean_s = sum / (double)cnt;  // replay-order sum (the reference sums the sorted samples)
+        ls.p50_s = q[0];
+        ls.p95_s = q[1];
+        ls.p99_s = q[2];
+        ls.max_s = q[3];
+      };
+      fill(m.ttft_completion, nc[p], o.sum_ttft_completion, st);
+      fill(m.e2e_reasoning, nr[p] - nc[p], o.sum_e2e_reasoning, st + 4);
     }
     if (summaries && n_scenarios > 0) std::memcpy(summaries, summ.data(), n_scenarios * sizeof(cace_summary_t));
+    pt.mark("post");
     for (int64_t i = 0; i < n_scenarios; ++i)
       if (metrics[i].status != CACE_OK) {
         put_msg(msg, msg_cap, status_text(e->cat, metrics[i].status));
@@ -922,6 +1014,7 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     return CACE_OK;
   });
   cace_engine_destroy(e);
+  pt.mark("destroy");
   return rc;
 }
 

@@ -18,7 +18,7 @@
 namespace cace {
 
 struct MetricsParams {
-  const double* samples;   // batch sample buffer
+  double* samples;         // batch sample buffer (the select compacts it in place)
   const int64_t* off;      // [B] first sample of batch scenario b
   const uint32_t* ncomp;   // [B] completion requests of b's trace
   const uint32_t* nreq;    // [B] requests of b's trace
@@ -36,13 +36,50 @@ __host__ __device__ inline uint32_t nearest_rank0(double q, uint32_t n) {
 
 constexpr int METRICS_BLOCK = 256;
 constexpr int METRICS_LIST = 5120;  // keys kept in shared memory once the prefixes are narrow
+constexpr int METRICS_UNROLL = 8;   // keys per thread per tile
+
+// Selected digit bookkeeping, one warp per target (see the kernel).
+__device__ inline void metrics_place(const uint32_t* h, int lane, uint32_t* krem, uint64_t* prefix,
+                                     uint32_t* cnt, int shift) {
+  uint32_t c[8], sum = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c[j] = h[lane * 8 + j];
+    sum += c[j];
+  }
+  uint32_t incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t excl = incl - sum;
+  const uint32_t k = *krem;
+  __syncwarp();  // every lane has read krem before one lane rewrites it
+  if (k >= excl && k < incl) {  // exactly one lane holds rank k's bin
+    uint32_t cum = excl;
+    int d = -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (d < 0) {
+        if (k < cum + c[j])
+          d = j;
+        else
+          cum += c[j];
+      }
+    }
+    *krem = k - cum;
+    *prefix |= (uint64_t)(lane * 8 + d) << shift;
+    *cnt = c[d];  // keys under the extended prefix
+  }
+}
 
 __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsParams P) {
   const int seg = blockIdx.x;  // 2 * b + class
   const int b = seg >> 1, cls = seg & 1;
   const uint32_t nc = P.ncomp[b], n = P.nreq[b];
   const uint32_t len = cls ? n - nc : nc;
-  const uint64_t* x = reinterpret_cast<const uint64_t*>(P.samples + P.off[b] + (cls ? nc : 0));
+  // the segment is this CTA's own: later passes compact it in place
+  uint64_t* x = reinterpret_cast<uint64_t*>(P.samples + P.off[b] + (cls ? nc : 0));
   double* out = P.stat + (size_t)seg * 4;
   if (len == 0) {  // compute_run_metrics throws; the host reports it
     if (threadIdx.x < 4) out[threadIdx.x] = 0.0;
@@ -58,118 +95,108 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
   __shared__ uint64_t s_list[METRICS_LIST];  // keys matching a target prefix (after compaction)
   __shared__ uint32_t s_nlist;
 
-  // max (the last order statistic) by reduction
-  uint64_t mx = 0;
-  for (uint32_t i = threadIdx.x; i < len; i += METRICS_BLOCK) mx = max(mx, x[i]);
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_max[warp] = mx;
   if (threadIdx.x < 3) {
     const double q = threadIdx.x == 0 ? 0.50 : (threadIdx.x == 1 ? 0.95 : 0.99);
     s_krem[threadIdx.x] = nearest_rank0(q, len);
     s_prefix[threadIdx.x] = 0;
+    s_cnt[threadIdx.x] = len;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t m = s_max[0];
-    for (int w = 1; w < METRICS_BLOCK / 32; ++w) m = max(m, s_max[w]);
-    out[3] = __longlong_as_double((long long)m);
-  }
 
-  // The passes read the segment from global memory until the targets'
-  // prefixes are narrow enough that every key matching one of them fits in
-  // shared memory; those keys are then compacted once and the remaining
-  // passes run on the shared list.
-  const uint64_t* src = x;
+  // MSD passes.  Keys under the targets' current prefixes (the selected bins
+  // of the previous pass, `need` of them) are the only ones later passes
+  // look at, so the working set shrinks as soon as it pays:
+  //  * need <= METRICS_LIST: copied once into shared memory;
+  //  * need <= half the working set: compacted in place in global memory
+  //    during the pass (tiles are read completely before any of their keys
+  //    is written back, and a key is only written at a position that has
+  //    already been read), which handles heavy bins of identical samples.
+  // The max (last order statistic) is reduced during the first pass.
+  uint64_t* src = x;
   uint32_t slen = len;
-  bool compacted = false;
+  bool in_smem = false;
+  uint64_t mx = 0;
   for (int shift = 56; shift >= 0; shift -= 8) {
     const uint64_t mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-    if (!compacted && shift <= 40) {
-      // total keys under the (distinct) current prefixes = the selected bins
-      // of the previous pass: compact if they fit
+    const uint64_t q0 = s_prefix[0], q1 = s_prefix[1], q2 = s_prefix[2];
+    const uint32_t need = s_cnt[0] + (q1 != q0 ? s_cnt[1] : 0u) + (q2 != q0 && q2 != q1 ? s_cnt[2] : 0u);
+    bool compact = false;
+    if (shift < 56 && !in_smem && need <= (uint32_t)METRICS_LIST) {
       if (threadIdx.x == 0) s_nlist = 0;
       __syncthreads();
-      const uint64_t r0 = s_prefix[0], r1 = s_prefix[1], r2 = s_prefix[2];
-      const uint32_t need = s_cnt[0] + (r1 != r0 ? s_cnt[1] : 0u) + (r2 != r0 && r2 != r1 ? s_cnt[2] : 0u);
-      if (need <= (uint32_t)METRICS_LIST) {
-        const uint64_t q0 = s_prefix[0], q1 = s_prefix[1], q2 = s_prefix[2];
-        for (uint32_t i = threadIdx.x; i < len; i += METRICS_BLOCK) {
-          const uint64_t v = x[i];
-          const uint64_t pv = v & mask;
-          if (pv == q0 || pv == q1 || pv == q2) s_list[atomicAdd(&s_nlist, 1u)] = v;
-        }
-        __syncthreads();
-        src = s_list;
-        slen = s_nlist;
-        compacted = true;
+      for (uint32_t i = threadIdx.x; i < slen; i += METRICS_BLOCK) {
+        const uint64_t v = src[i];
+        const uint64_t pv = v & mask;
+        if (pv == q0 || pv == q1 || pv == q2) s_list[atomicAdd(&s_nlist, 1u)] = v;
       }
+      __syncthreads();
+      src = s_list;
+      slen = s_nlist;
+      in_smem = true;
+    } else if (shift < 56 && !in_smem && need <= slen / 2) {
+      compact = true;
     }
     if (threadIdx.x < 3) {
       const int t = threadIdx.x;
-      int src = t;
+      int sr = t;
       for (int u = 0; u < t; ++u)
         if (s_prefix[u] == s_prefix[t]) {
-          src = u;
+          sr = u;
           break;
         }
-      s_src[t] = src;
+      s_src[t] = sr;
     }
+    if (compact && threadIdx.x == 0) s_nlist = 0;  // (not after the shared copy: slen was just read from it)
     for (int i = threadIdx.x; i < 3 * 256; i += METRICS_BLOCK) (&hist[0][0])[i] = 0;
     __syncthreads();
-    const uint64_t p0 = s_prefix[0], p1 = s_prefix[1], p2 = s_prefix[2];
     const bool d1 = s_src[1] == 1, d2 = s_src[2] == 2;  // distinct histograms needed
-    for (uint32_t i0 = 0; i0 < slen; i0 += METRICS_BLOCK) {
-      const uint32_t i = i0 + threadIdx.x;
-      const unsigned act = __ballot_sync(0xffffffffu, i < slen);
-      if (i < slen) {
-        const uint64_t v = src[i];
-        const int d = (int)((v >> shift) & 255u);
-        const uint64_t pv = v & mask;
-        // one histogram per distinct prefix; lanes with the same bin add once
-        const int bin0 = pv == p0 ? d : -1;
-        const int bin1 = d1 && pv == p1 ? d : -1;
-        const int bin2 = d2 && pv == p2 ? d : -1;
-        const int key = (bin0 >= 0 ? bin0 : (bin1 >= 0 ? 256 + bin1 : (bin2 >= 0 ? 512 + bin2 : -1)));
-        const unsigned peers = __match_any_sync(act, key);
-        if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&(&hist[0][0])[key], (uint32_t)__popc(peers));
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (uint32_t base = 0; base < slen; base += METRICS_BLOCK * METRICS_UNROLL) {
+      uint64_t v[METRICS_UNROLL];
+#pragma unroll
+      for (int u = 0; u < METRICS_UNROLL; ++u) {
+        const uint32_t i = base + u * METRICS_BLOCK + threadIdx.x;
+        v[u] = i < slen ? src[i] : 0ull;
       }
+      if (compact) __syncthreads();  // the whole tile is read before any write-back
+#pragma unroll
+      for (int u = 0; u < METRICS_UNROLL; ++u) {
+        const bool valid = base + u * METRICS_BLOCK + threadIdx.x < slen;
+        const unsigned act = __ballot_sync(0xffffffffu, valid);
+        if (!act) continue;
+        const uint64_t pv = v[u] & mask;
+        const bool hit0 = pv == q0, hit1 = d1 && pv == q1, hit2 = d2 && pv == q2;
+        if (valid) {
+          if (shift == 56) mx = max(mx, v[u]);
+          // one histogram per distinct prefix; lanes with the same bin add once
+          const int d = (int)((v[u] >> shift) & 255u);
+          const int key = hit0 ? d : (hit1 ? 256 + d : (hit2 ? 512 + d : -1));
+          const unsigned peers = __match_any_sync(act, key);
+          if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&(&hist[0][0])[key], (uint32_t)__popc(peers));
+        }
+        if (compact) {
+          const bool keep = valid && (pv == q0 || pv == q1 || pv == q2);
+          const unsigned bal = __ballot_sync(0xffffffffu, keep);
+          uint32_t wb = 0;
+          if (lane == 0 && bal) wb = atomicAdd(&s_nlist, (uint32_t)__popc(bal));
+          wb = __shfl_sync(0xffffffffu, wb, 0);
+          if (keep) src[wb + __popc(bal & lt_mask)] = v[u];
+        }
+      }
+    }
+    if (shift == 56) {
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) s_max[warp] = mx;
     }
     __syncthreads();
-    // digit of each target: warp t scans its (shared) histogram
-    if (warp < 3) {
-      const int t = warp;
-      const uint32_t* h = hist[s_src[t]];
-      uint32_t c[8], sum = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = h[lane * 8 + j];
-        sum += c[j];
-      }
-      uint32_t incl = sum;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t excl = incl - sum;
-      const uint32_t k = s_krem[t];
-      __syncwarp();  // every lane has read s_krem[t] before one lane rewrites it
-      if (k >= excl && k < incl) {  // exactly one lane holds rank k's bin
-        uint32_t cum = excl;
-        int d = -1;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (d < 0) {
-            if (k < cum + c[j])
-              d = j;
-            else
-              cum += c[j];
-          }
-        }
-        s_krem[t] = k - cum;
-        s_prefix[t] |= (uint64_t)(lane * 8 + d) << shift;
-        s_cnt[t] = c[d];  // keys under the extended prefix
-      }
+    if (shift == 56 && threadIdx.x == 0) {
+      uint64_t m = s_max[0];
+      for (int w = 1; w < METRICS_BLOCK / 32; ++w) m = max(m, s_max[w]);
+      out[3] = __longlong_as_double((long long)m);
     }
+    if (compact) slen = s_nlist;
+    // digit of each target: warp t scans its (shared) histogram
+    if (warp < 3) metrics_place(hist[s_src[warp]], lane, &s_krem[warp], &s_prefix[warp], &s_cnt[warp], shift);
     __syncthreads();
   }
   if (threadIdx.x < 3) out[threadIdx.x] = __longlong_as_double((long long)s_prefix[threadIdx.x]);

@@ -77,6 +77,35 @@ def test_run_metrics_config4_slice(ref):
     _check(ref, catalog, traces, sc[pick], got[pick], "cfg4 slice")
 
 
+def test_run_metrics_chunked_pipeline(ref, monkeypatch):
+    """A tiny sample budget cuts the sweep into one-warp chunks over the ring
+    buffers (cace_run_metrics_batch's pipeline): same records as one chunk
+    per segment, and bit-exact against the reference."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 20_000, seed=7 + s) for s in range(2)]
+    sc = synth.scenario_grid(synth.weight_vectors_cfg3()[::211], range(1, 9), 2,
+                             catalog.max_expected_output_tokens())
+    whole = P.run_metrics(traces, catalog, sc)
+    monkeypatch.setenv("CACE_METRICS_BUDGET_MB", "1")
+    chunked = P.run_metrics(traces, catalog, sc)
+    assert whole.tobytes() == chunked.tobytes()
+    pick = np.random.default_rng(5).choice(len(sc), 16, replace=False)
+    _check(ref, catalog, traces, sc[pick], chunked[pick], "chunked")
+
+
+def test_run_metrics_long_trace_heavy_bins(ref):
+    """100k requests: the select's working set is compacted in place in global
+    memory (more than METRICS_LIST keys under the targets' prefixes), including
+    bins of identical samples (no-eviction capacities: warm-hit TTFT = prefill)."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 100_000, seed=21)]
+    rows = [(0, PolicyConfig(variant=v, output_token_normalizer=600), ClusterConfig(num_accelerators=c))
+            for v in (api.Variant.LRU, api.Variant.CACE_FULL) for c in (1, 2, 3, 8)]
+    sc = api.make_scenarios(rows)
+    got = P.run_metrics(traces, catalog, sc)
+    _check(ref, catalog, traces, sc, got, "long trace")
+
+
 def test_run_metrics_errors_match_reference(ref):
     """compute_run_metrics' SimErrors (metrics.cpp:37-58): empty report, no
     completion outcomes, no reasoning outcomes."""
