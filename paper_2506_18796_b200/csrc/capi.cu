@@ -27,6 +27,16 @@ using namespace cace;
 
 namespace {
 
+// The engine drives up to 17 streams (engine stream, 8 workers, 8 select
+// streams); with CUDA's default 8 hardware work queues, streams alias onto
+// shared queues and independent launches serialise behind each other's waits.
+// Raise the queue count at library load unless the user set it (effective
+// only if this process has not created its CUDA context yet).
+const int g_connections = [] {
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+  return 0;
+}();
+
 const double kLogTab[256] = CACE_GLIBC_LOG_TAB;
 const double kLogTab2[256] = CACE_GLIBC_LOG_TAB2;
 
@@ -542,7 +552,7 @@ void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams 
   if (g.warp)
     dispatch_warp(dump_on, g.C, P, end - b, ws);
   else
-    dispatch_lane(dump_on, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C), ws, latency);
+    dispatch_lane(dump_on, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, latency);
 }
 
 void fill_status(cace_engine* e, cace_summary_t* d_out, cudaStream_t s) {
@@ -896,7 +906,12 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
           int64_t ub = 0;
           for (int64_t q = c.e; q < ue; ++q)
             if (!(order[q] & (int64_t)kShadowBit)) ub += nreq(order[q]);
-          if (c.e > c.b && (size_t)(c.nsamp + ub) * 8 > per) break;
+          // the first chunk of ring r is (r + 1) / W of full size, which puts
+          // the rings out of phase: their selects (memory-bound) then overlap
+          // other rings' replays (latency-bound) instead of all falling
+          // between two rounds of replays
+          const size_t lim = chunks.size() < W ? per / W * (chunks.size() + 1) : per;
+          if (c.e > c.b && (size_t)(c.nsamp + ub) * 8 > lim) break;
           for (int64_t q = c.e; q < ue; ++q) {
             if (order[q] & (int64_t)kShadowBit) continue;
             const int64_t si = order[q];
@@ -940,23 +955,67 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     dd.slot = d_slot.p;
     const ReplayParams P0 = replay_params(e, d_sc.p, d_out.p, dd);
     e->last_launches = 0;
+    // Selects run on their own high-priority streams: the block scheduler
+    // then places their CTAs ahead of queued replay blocks as SMs free up,
+    // which returns ring buffers sooner.  Per ring r: replay (worker r, after
+    // the previous select of r) -> select (select stream r).
+    struct StreamSet {
+      std::vector<cudaStream_t> st;
+      std::vector<cudaEvent_t> rep, sel;
+      ~StreamSet() {
+        for (auto x : st) cudaStreamDestroy(x);
+        for (auto x : rep) cudaEventDestroy(x);
+        for (auto x : sel) cudaEventDestroy(x);
+      }
+    } ss;
+    int prio_lo = 0, prio_hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const size_t nring = std::min(W, chunks.size());
+    for (size_t r = 0; r < nring; ++r) {
+      cudaStream_t x;
+      cudaEvent_t a, b;
+      CK(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_hi));
+      ss.st.push_back(x);
+      CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      ss.rep.push_back(a);
+      CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      ss.sel.push_back(b);
+    }
+    // CACE_TIMING: per-chunk device timeline (replay start / end, select end)
+    std::vector<cudaEvent_t> tl;
+    if (pt.on)
+      for (size_t j = 0; j < 3 * chunks.size() + 1; ++j) {
+        cudaEvent_t x;
+        CK(cudaEventCreate(&x));
+        tl.push_back(x);
+      }
+    if (pt.on) CK(cudaEventRecord(tl.back(), s));
     fork_workers(e, s, chunks.size());
     for (size_t j = 0; j < chunks.size(); ++j) {
       const Chunk& c = chunks[j];
-      cudaStream_t ws = e->workers[j % W];
+      const size_t r = j % W;
+      cudaStream_t ws = e->workers[r];
+      if (j >= W) CK(cudaStreamWaitEvent(ws, ss.sel[r], 0));  // ring r is free again
+      if (pt.on) CK(cudaEventRecord(tl[3 * j], ws));
       ReplayParams P = P0;
       P.dump.dump_off = d_off.p + c.base;
-      P.dump.samples = ring[j % W].p;
+      P.dump.samples = ring[r].p;
       launch_piece(e, e->segs[c.seg], P, c.b, c.e, ws, false);
       ++e->last_launches;
+      CK(cudaEventRecord(ss.rep[r], ws));
+      if (pt.on) CK(cudaEventRecord(tl[3 * j + 1], ws));
+      CK(cudaStreamWaitEvent(ss.st[r], ss.rep[r], 0));
       if (c.nloc > 0) {
-        MetricsParams mp{ring[j % W].p, d_off.p + c.base, d_nc.p + c.base, d_nr.p + c.base,
+        MetricsParams mp{ring[r].p, d_off.p + c.base, d_nc.p + c.base, d_nr.p + c.base,
                          d_stat.p + (size_t)c.base * 8};
-        metrics_select_kernel<<<(unsigned)(2 * c.nloc), METRICS_BLOCK, 0, ws>>>(mp);
+        metrics_select_kernel<<<(unsigned)(2 * c.nloc), METRICS_BLOCK, 0, ss.st[r]>>>(mp);
         CK(cudaGetLastError());
         ++e->last_launches;
       }
+      CK(cudaEventRecord(ss.sel[r], ss.st[r]));
+      if (pt.on) CK(cudaEventRecord(tl[3 * j + 2], ss.st[r]));
     }
+    for (size_t r = 0; r < nring; ++r) CK(cudaStreamWaitEvent(s, ss.sel[r], 0));
     join_workers(e, s, chunks.size());
     fill_status(e, d_out.p, s);
     std::vector<cace_summary_t> summ(n_scenarios);
@@ -966,6 +1025,17 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     if (NL > 0) CK(cudaMemcpyAsync(stat.data(), d_stat.p, (size_t)NL * 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     pt.mark("replay+select");
+    if (pt.on) {
+      for (size_t j = 0; j < chunks.size(); ++j) {
+        float a = 0, b = 0, d = 0;
+        cudaEventElapsedTime(&a, tl.back(), tl[3 * j]);
+        cudaEventElapsedTime(&b, tl.back(), tl[3 * j + 1]);
+        cudaEventElapsedTime(&d, tl.back(), tl[3 * j + 2]);
+        std::fprintf(stderr, "cace_chunk %3zu ring %zu C %2d n %6lld  replay %8.2f -> %8.2f  select -> %8.2f ms\n", j,
+                     j % W, e->segs[chunks[j].seg].C, (long long)chunks[j].nloc, a, b, d);
+      }
+      for (auto x : tl) cudaEventDestroy(x);
+    }
     for (auto& r : ring) r.release();
     // RunMetrics (compute_run_metrics, metrics.cpp:35-62)
     std::vector<int64_t> pos(n_scenarios, -1);

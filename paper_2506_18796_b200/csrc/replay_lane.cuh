@@ -322,7 +322,30 @@ struct LaneSmem {
   int stride;
   ReqRec* rec;       // warp: record double buffer [64]
   WinEnt* win;       // warp: window table [M]
+  double* samp;      // warp: metrics sample tile [2 classes][kSampT][32 lanes] (DUMP only)
 };
+
+// Metrics samples leave through a per-warp shared tile: the lanes of a warp
+// replay the same trace in lockstep, so request k has the same class-local
+// index ci in every lane; kSampT consecutive samples per lane are gathered and
+// written as kSampT * 8 contiguous bytes per scenario (32 / kSampT scenarios
+// per store instruction) instead of 32 scattered 8-B stores per request.
+constexpr int kSampT = 4;
+
+#ifndef CACE_HOST_EMULATION
+// Warp-collective: lane q's tile column [0, cnt) -> mine(q)[base + 0 .. cnt).
+__device__ __forceinline__ void flush_samples(const double* tile, double* mine, int64_t base, int cnt) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane % kSampT;
+#pragma unroll
+  for (int i = 0; i < kSampT; ++i) {
+    const int q = lane / kSampT + (32 / kSampT) * i;
+    const double v = tile[j * 32 + q];
+    double* pq = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), q));
+    if (pq && j < cnt) pq[base + j] = v;
+  }
+}
+#endif
 
 // Replays one scenario (see the file comment).  shadow lanes (warp padding)
 // replay a copy of a real scenario for lockstep and write nothing.
@@ -385,8 +408,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     dump_outcomes = P.dump.cold || P.dump.queue_wait || P.dump.load_wait || P.dump.prefill ||
                     P.dump.decode || P.dump.ttft || P.dump.e2e;
     if (dslot >= 0 && P.dump.samples) samples = P.dump.samples + doff;
-    ncomp_t = P.trace_ncomp[sc.trace];
   }
+  if (DUMP) ncomp_t = P.trace_ncomp[sc.trace];  // shadows too: the sample tile flush is collective
   RecStream rs;
   rs.init(tr, n, S.rec);
   Window<MW> win;
@@ -699,13 +722,27 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         if (P.dump.ttft) P.dump.ttft[o] = ttft;
         if (P.dump.e2e) P.dump.e2e[o] = e2e;
       }
-      // metrics samples (compute_run_metrics, metrics.cpp:44-52): TTFT of
-      // completion requests, then E2E of reasoning requests
-      if (samples) {
-        const bool comp = (mc >> 16) == CACE_COMPLETION;
-        samples[comp ? R.ci : ncomp_t + R.ci] = comp ? ttft : e2e;
+    }
+    // metrics samples (compute_run_metrics, metrics.cpp:44-52): TTFT of
+    // completion requests, then E2E of reasoning requests
+#ifndef CACE_HOST_EMULATION
+    if (DUMP && P.dump.samples) {  // warp-collective (shadow lanes take part, write nothing)
+      const bool comp = (mc >> 16) == CACE_COMPLETION;
+      const uint32_t ci = R.ci;
+      double* tc = S.samp + (comp ? 0 : kSampT * 32);
+      tc[(ci % kSampT) * 32 + (threadIdx.x & 31)] = comp ? ttft : e2e;
+      if (ci % kSampT == kSampT - 1) {
+        __syncwarp();
+        flush_samples(tc, samples, (int64_t)(comp ? 0 : ncomp_t) + ci - (kSampT - 1), kSampT);
+        __syncwarp();
       }
     }
+#else
+    if (DUMP && samples) {
+      const bool comp = (mc >> 16) == CACE_COMPLETION;
+      samples[comp ? R.ci : ncomp_t + R.ci] = comp ? ttft : e2e;
+    }
+#endif
     if (C > 1 && warp_win) {  // the head leaves the window (collective)
       win.prepare(m, R.nxt);
       win.commit(R.nxa);
@@ -713,6 +750,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   }
   }
 
+#ifndef CACE_HOST_EMULATION
+  if (DUMP && P.dump.samples) {  // partial tiles
+    const uint32_t nco = ncomp_t, nre = n - ncomp_t;
+    __syncwarp();
+    if (nco % kSampT) flush_samples(S.samp, samples, nco - nco % kSampT, nco % kSampT);
+    if (nre % kSampT)
+      flush_samples(S.samp + kSampT * 32, samples, (int64_t)ncomp_t + nre - nre % kSampT, nre % kSampT);
+  }
+#endif
   if (shadow) return;
   cace_summary_t o;
   o.hits = hits;
@@ -750,10 +796,12 @@ inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 *
 inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
   return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + 4 * 4 + C * 8 + M);
 }
-inline __host__ __device__ size_t lane_smem_warp(int M) { return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt); }
-inline size_t lane_smem_bytes(int M, int C) {
+inline __host__ __device__ size_t lane_smem_warp(int M, bool dump) {
+  return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? 2 * kSampT * 32 * sizeof(double) : 0);
+}
+inline size_t lane_smem_bytes(int M, int C, bool dump) {
   const size_t a = (((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
-  return a + (LANE_BLOCK / 32) * lane_smem_warp(M);
+  return a + (LANE_BLOCK / 32) * lane_smem_warp(M, dump);
 }
 
 // MINB = resident blocks per SM the register allocation targets:
@@ -783,9 +831,10 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_word + (size_t)C * LANE_BLOCK);  // [M][LANE_BLOCK]
   unsigned char* wbase =
       smem + ((((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
-      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M);
+      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DUMP);
   ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
   WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
+  double* w_samp = reinterpret_cast<double*>(w_win + M);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
@@ -808,7 +857,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x, l_prm + threadIdx.x,
                    l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
-                   w_rec, w_win};
+                   w_rec, w_win, w_samp};
   replay_scenario<C, MW, DUMP, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
 }
 #endif  // CACE_HOST_EMULATION

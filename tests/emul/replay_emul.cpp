@@ -53,7 +53,7 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   std::vector<uint32_t> seq(C);
   std::vector<int> word(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), p4d.data(), done.data(), prm.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr};
+  const LaneSmem S{p4f.data(), p4d.data(), done.data(), prm.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr, nullptr};
   if (g_xr)
     replay_scenario<C, 2, D, true>(P, i, false, need_win, K, S);
   else
