@@ -906,12 +906,7 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
           int64_t ub = 0;
           for (int64_t q = c.e; q < ue; ++q)
             if (!(order[q] & (int64_t)kShadowBit)) ub += nreq(order[q]);
-          // the first chunk of ring r is (r + 1) / W of full size, which puts
-          // the rings out of phase: their selects (memory-bound) then overlap
-          // other rings' replays (latency-bound) instead of all falling
-          // between two rounds of replays
-          const size_t lim = chunks.size() < W ? per / W * (chunks.size() + 1) : per;
-          if (c.e > c.b && (size_t)(c.nsamp + ub) * 8 > lim) break;
+          if (c.e > c.b && (size_t)(c.nsamp + ub) * 8 > per) break;
           for (int64_t q = c.e; q < ue; ++q) {
             if (order[q] & (int64_t)kShadowBit) continue;
             const int64_t si = order[q];
