@@ -73,6 +73,70 @@ __device__ inline void metrics_place(const uint32_t* h, int lane, uint32_t* krem
   }
 }
 
+// One histogram pass over src[0, slen).  FIRST: the first pass (empty
+// prefixes: the digit is the key's top byte; also reduces the max).  HI32:
+// shift >= 32, so prefixes and digit live in the high word (32-bit compares).
+// COMPACT: keys under a target prefix are written back in place (see the
+// kernel).  Lanes with equal bins add once (__match_any_sync).
+template <bool FIRST, bool HI32, bool COMPACT>
+__device__ __forceinline__ void metrics_pass(uint64_t* src, uint32_t slen, int shift, uint64_t mask,
+                                             uint64_t q0, uint64_t q1, uint64_t q2, bool d1, bool d2,
+                                             uint32_t* hist, uint32_t* nlist, uint64_t& mx) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint32_t mh = (uint32_t)(mask >> 32);
+  const uint32_t h0 = (uint32_t)(q0 >> 32), h1 = (uint32_t)(q1 >> 32), h2 = (uint32_t)(q2 >> 32);
+  for (uint32_t base = 0; base < slen; base += METRICS_BLOCK * METRICS_UNROLL) {
+    uint64_t v[METRICS_UNROLL];
+#pragma unroll
+    for (int u = 0; u < METRICS_UNROLL; ++u) {
+      const uint32_t i = base + u * METRICS_BLOCK + threadIdx.x;
+      v[u] = i < slen ? src[i] : 0ull;
+    }
+    if (COMPACT) __syncthreads();  // the whole tile is read before any write-back
+#pragma unroll
+    for (int u = 0; u < METRICS_UNROLL; ++u) {
+      const bool valid = base + u * METRICS_BLOCK + threadIdx.x < slen;
+      const unsigned act = __ballot_sync(0xffffffffu, valid);
+      if (!act) continue;
+      bool m0, m1, m2;
+      int d;
+      if (FIRST) {
+        m0 = true;
+        m1 = m2 = false;
+        d = (int)(v[u] >> 56);
+      } else if (HI32) {
+        const uint32_t ph = (uint32_t)(v[u] >> 32) & mh;
+        m0 = ph == h0;
+        m1 = ph == h1;
+        m2 = ph == h2;
+        d = (int)(((uint32_t)(v[u] >> 32) >> (shift - 32)) & 255u);
+      } else {
+        const uint64_t pv = v[u] & mask;
+        m0 = pv == q0;
+        m1 = pv == q1;
+        m2 = pv == q2;
+        d = (int)((v[u] >> shift) & 255u);
+      }
+      if (valid) {
+        if (FIRST) mx = max(mx, v[u]);
+        // one histogram per distinct prefix; lanes with the same bin add once
+        const int key = m0 ? d : ((d1 && m1) ? 256 + d : ((d2 && m2) ? 512 + d : -1));
+        const unsigned peers = __match_any_sync(act, key);
+        if (key >= 0 && (peers & lt_mask) == 0) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+      }
+      if (COMPACT) {
+        const bool keep = valid && (m0 || m1 || m2);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        uint32_t wb = 0;
+        if (lane == 0 && bal) wb = atomicAdd(nlist, (uint32_t)__popc(bal));
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if (keep) src[wb + __popc(bal & lt_mask)] = v[u];
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsParams P) {
   const int seg = blockIdx.x;  // 2 * b + class
   const int b = seg >> 1, cls = seg & 1;
@@ -124,10 +188,19 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
     if (shift < 56 && !in_smem && need <= (uint32_t)METRICS_LIST) {
       if (threadIdx.x == 0) s_nlist = 0;
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < slen; i += METRICS_BLOCK) {
-        const uint64_t v = src[i];
-        const uint64_t pv = v & mask;
-        if (pv == q0 || pv == q1 || pv == q2) s_list[atomicAdd(&s_nlist, 1u)] = v;
+      for (uint32_t base = 0; base < slen; base += METRICS_BLOCK * 4) {
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = base + u * METRICS_BLOCK + threadIdx.x;
+          v[u] = i < slen ? src[i] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t pv = v[u] & mask;
+          if (base + u * METRICS_BLOCK + threadIdx.x < slen && (pv == q0 || pv == q1 || pv == q2))
+            s_list[atomicAdd(&s_nlist, 1u)] = v[u];
+        }
       }
       __syncthreads();
       src = s_list;
@@ -150,40 +223,15 @@ __global__ void __launch_bounds__(METRICS_BLOCK) metrics_select_kernel(MetricsPa
     for (int i = threadIdx.x; i < 3 * 256; i += METRICS_BLOCK) (&hist[0][0])[i] = 0;
     __syncthreads();
     const bool d1 = s_src[1] == 1, d2 = s_src[2] == 2;  // distinct histograms needed
-    const unsigned lt_mask = (1u << lane) - 1u;
-    for (uint32_t base = 0; base < slen; base += METRICS_BLOCK * METRICS_UNROLL) {
-      uint64_t v[METRICS_UNROLL];
-#pragma unroll
-      for (int u = 0; u < METRICS_UNROLL; ++u) {
-        const uint32_t i = base + u * METRICS_BLOCK + threadIdx.x;
-        v[u] = i < slen ? src[i] : 0ull;
-      }
-      if (compact) __syncthreads();  // the whole tile is read before any write-back
-#pragma unroll
-      for (int u = 0; u < METRICS_UNROLL; ++u) {
-        const bool valid = base + u * METRICS_BLOCK + threadIdx.x < slen;
-        const unsigned act = __ballot_sync(0xffffffffu, valid);
-        if (!act) continue;
-        const uint64_t pv = v[u] & mask;
-        const bool hit0 = pv == q0, hit1 = d1 && pv == q1, hit2 = d2 && pv == q2;
-        if (valid) {
-          if (shift == 56) mx = max(mx, v[u]);
-          // one histogram per distinct prefix; lanes with the same bin add once
-          const int d = (int)((v[u] >> shift) & 255u);
-          const int key = hit0 ? d : (hit1 ? 256 + d : (hit2 ? 512 + d : -1));
-          const unsigned peers = __match_any_sync(act, key);
-          if (key >= 0 && lane == __ffs(peers) - 1) atomicAdd(&(&hist[0][0])[key], (uint32_t)__popc(peers));
-        }
-        if (compact) {
-          const bool keep = valid && (pv == q0 || pv == q1 || pv == q2);
-          const unsigned bal = __ballot_sync(0xffffffffu, keep);
-          uint32_t wb = 0;
-          if (lane == 0 && bal) wb = atomicAdd(&s_nlist, (uint32_t)__popc(bal));
-          wb = __shfl_sync(0xffffffffu, wb, 0);
-          if (keep) src[wb + __popc(bal & lt_mask)] = v[u];
-        }
-      }
-    }
+    uint32_t* hf = &hist[0][0];
+    if (shift == 56)
+      metrics_pass<true, true, false>(src, slen, shift, mask, q0, q1, q2, d1, d2, hf, &s_nlist, mx);
+    else if (shift >= 32)
+      compact ? metrics_pass<false, true, true>(src, slen, shift, mask, q0, q1, q2, d1, d2, hf, &s_nlist, mx)
+              : metrics_pass<false, true, false>(src, slen, shift, mask, q0, q1, q2, d1, d2, hf, &s_nlist, mx);
+    else
+      compact ? metrics_pass<false, false, true>(src, slen, shift, mask, q0, q1, q2, d1, d2, hf, &s_nlist, mx)
+              : metrics_pass<false, false, false>(src, slen, shift, mask, q0, q1, q2, d1, d2, hf, &s_nlist, mx);
     if (shift == 56) {
       for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) s_max[warp] = mx;
