@@ -985,6 +985,8 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
         tl.push_back(x);
       }
     if (pt.on) CK(cudaEventRecord(tl.back(), s));
+    // speculative first select digit (CACE_METRICS_SPEC: 0 off, 2 = test hook)
+    const int metrics_spec = std::getenv("CACE_METRICS_SPEC") ? std::atoi(std::getenv("CACE_METRICS_SPEC")) : 1;
     fork_workers(e, s, chunks.size());
     for (size_t j = 0; j < chunks.size(); ++j) {
       const Chunk& c = chunks[j];
@@ -1002,7 +1004,7 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
       CK(cudaStreamWaitEvent(ss.st[r], ss.rep[r], 0));
       if (c.nloc > 0) {
         MetricsParams mp{ring[r].p, d_off.p + c.base, d_nc.p + c.base, d_nr.p + c.base,
-                         d_stat.p + (size_t)c.base * 8};
+                         d_stat.p + (size_t)c.base * 8, metrics_spec};
         metrics_select_kernel<<<(unsigned)(2 * c.nloc), METRICS_BLOCK, 0, ss.st[r]>>>(mp);
         CK(cudaGetLastError());
         ++e->last_launches;

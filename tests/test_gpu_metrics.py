@@ -106,6 +106,24 @@ def test_run_metrics_long_trace_heavy_bins(ref):
     _check(ref, catalog, traces, sc, got, "long trace")
 
 
+def test_run_metrics_speculative_digit_paths(ref, monkeypatch):
+    """The select's speculative first digit (segments >= 16384 samples): on,
+    off, and with every guess forced wrong (CACE_METRICS_SPEC=2, the fallback
+    path) give identical records, bit-exact against the reference."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 60_000, seed=33, bursty=True)]
+    rows = [(0, PolicyConfig(variant=v, output_token_normalizer=600, window_length=w), ClusterConfig(num_accelerators=c))
+            for v in (api.Variant.LRU, api.Variant.CACE_FULL) for c in (1, 3, 8) for w in (2, 10)]
+    sc = api.make_scenarios(rows)
+    res = {}
+    for mode in ("1", "0", "2"):
+        monkeypatch.setenv("CACE_METRICS_SPEC", mode)
+        res[mode] = P.run_metrics(traces, catalog, sc)
+    assert res["1"].tobytes() == res["0"].tobytes()
+    assert res["2"].tobytes() == res["0"].tobytes()
+    _check(ref, catalog, traces, sc, res["1"], "speculative select")
+
+
 def test_run_metrics_errors_match_reference(ref):
     """compute_run_metrics' SimErrors (metrics.cpp:37-58): empty report, no
     completion outcomes, no reasoning outcomes."""
