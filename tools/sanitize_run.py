@@ -27,4 +27,19 @@ for catalog in (synth.eight_model_catalog(), api.ModelCatalog.synthetic_pool(80,
         assert (a["outcome_hash"] == b["outcome_hash"]).all()
     m = P.run_metrics(traces, catalog, sc, raise_on_error=False)
     assert (m["status"] == 0).all()
+# RunMetrics on a trace long enough for the select's speculative digit and
+# in-place compaction (> 16384 completion samples), chunked over the ring
+# buffers, with the speculation both taken and forced to miss
+catalog = synth.eight_model_catalog()
+traces = [synth.mixed_trace(catalog, 25_000, seed=5)]
+rows = [(0, PolicyConfig(variant=v, window_length=10), ClusterConfig(num_accelerators=c))
+        for v in (0, 1) for c in (1, 3, 8)]
+sc = api.make_scenarios(rows)
+os.environ["CACE_METRICS_BUDGET_MB"] = "1"
+ref_m = None
+for mode in ("1", "2"):
+    os.environ["CACE_METRICS_SPEC"] = mode
+    m = P.run_metrics(traces, catalog, sc)
+    ref_m = m if ref_m is None else ref_m
+    assert m.tobytes() == ref_m.tobytes()
 print("sanitize run ok")
