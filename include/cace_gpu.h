@@ -18,6 +18,7 @@
  *   cace_log_selftest        <- the libm log the reference calls             policy.cpp:51
  *   cace_run_metrics_batch   <- RunMetrics compute_run_metrics(const SimulationReport&)
  *                               for every replay of a sweep                 metrics.hpp:29-31
+ *   cace_metrics_select      <- LatencySummary summarize(std::vector<double>) metrics.cpp:14-33
  *   cace_trace_parse_jsonl   <- Trace parse_trace(const std::string&)        workload.hpp:71
  *   cace_trace_load_jsonl    <- Trace load_trace(const std::string& path)    workload.hpp:73
  *
@@ -213,14 +214,27 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
  * from the replay summary.  count, percentiles, max, hit rate, load overhead
  * and evictions are bit-identical to the reference; mean_s divides the
  * replay-order sum (the reference sums the sorted samples, metrics.cpp:26), so
- * it agrees to ~1e-15 relative.  Scenarios are processed in batches sized to
- * the free device memory.  summaries (optional, NULL) receives the replay
- * summaries too.  Host memory. */
+ * it agrees to ~1e-15 relative.  The sweep is replayed in chunks pipelined
+ * with their selects over ring buffers sized to the free device memory.
+ * summaries (optional, NULL) receives the replay summaries too.  Host memory. */
 int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
                                int32_t n_traces, const cace_scenario_t* scenarios,
                                int64_t n_scenarios, cace_run_metrics_t* metrics,
                                cace_summary_t* summaries, const cace_opts_t* opts, char* msg,
                                size_t msg_cap);
+
+/* The order-statistic step of compute_run_metrics alone (summarize,
+ * metrics.cpp:14-33: nearest-rank p50 / p95 / p99 and the max) over caller
+ * samples, through the same device select kernel the pipeline uses: segment
+ * b holds ncomp[b] TTFT samples then nreq[b] - ncomp[b] E2E samples starting
+ * at samples[off[b]] (latencies, >= +0).  stat[b * 8 + 4 * class + j] =
+ * {p50, p95, p99, max}[j]; an empty class yields zeros (the caller reports
+ * the reference's SimError).  spec: 1 speculative first digit (default
+ * pipeline behaviour), 0 off, 2 every speculation forced to miss (test hook).
+ * Host memory; the samples are copied (the kernel compacts its copy). */
+int32_t cace_metrics_select(const double* samples, const int64_t* off, const uint32_t* ncomp,
+                            const uint32_t* nreq, int64_t n_segments, double* stat, int32_t spec,
+                            const cace_opts_t* opts, char* msg, size_t msg_cap);
 
 /* Trace ingestion: the reference's JSONL trace format (serialize_trace,
  * workload.cpp:181-202) parsed with parse_trace's semantics and error texts

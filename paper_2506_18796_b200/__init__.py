@@ -23,6 +23,7 @@ from .api import (  # noqa: F401
     Trace,
     Variant,
     average_metrics,
+    metrics_select,
     dedup_window,
     device_count,
     eviction_score,

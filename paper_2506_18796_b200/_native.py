@@ -128,7 +128,7 @@ EXPORTED = [
     "cace_engine_create", "cace_engine_destroy", "cace_engine_plan", "cace_engine_replay_device",
     "cace_engine_status_message", "cace_engine_last_launches", "cace_select_victim_batch",
     "cace_eviction_score_batch", "cace_dedup_window_batch", "cace_service_times_batch",
-    "cace_log_selftest", "cace_log_host", "cace_probe_log_variant", "cace_run_metrics_batch",
+    "cace_log_selftest", "cace_log_host", "cace_probe_log_variant", "cace_run_metrics_batch", "cace_metrics_select",
     "cace_trace_parse_jsonl", "cace_trace_load_jsonl", "cace_trace_jsonl_size", "cace_trace_jsonl_header",
     "cace_trace_jsonl_copy", "cace_trace_jsonl_free",
 ]
@@ -151,6 +151,8 @@ def _load():
     L.cace_replay_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, P(DumpABI), P(OptsABI), C.c_char_p, sz]
     L.cace_run_metrics_batch.restype = i32
     L.cace_run_metrics_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, vp, P(OptsABI), C.c_char_p, sz]
+    L.cace_metrics_select.restype = i32
+    L.cace_metrics_select.argtypes = [vp, vp, vp, vp, i64, vp, i32, P(OptsABI), C.c_char_p, sz]
     L.cace_trace_parse_jsonl.restype = i32
     L.cace_trace_parse_jsonl.argtypes = [C.c_char_p, sz, P(vp), C.c_char_p, sz]
     L.cace_trace_load_jsonl.restype = i32

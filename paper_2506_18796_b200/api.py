@@ -497,6 +497,33 @@ def average_metrics(runs: np.ndarray) -> np.ndarray:
     return avg
 
 
+def metrics_select(segments, spec: int = 1, device: int = 0) -> np.ndarray:
+    """The nearest-rank order statistics of summarize (metrics.cpp:14-33) on
+    the device: segments = [(ttft_samples, e2e_samples), ...] (latencies >= 0)
+    -> float64 array [n, 2, 4] of {p50, p95, p99, max} per class (zeros for an
+    empty class).  Runs the select kernel of run_metrics (spec: 1 speculative
+    first digit, 0 off, 2 speculation forced to miss)."""
+    segs = [(np.ascontiguousarray(a, np.float64).ravel(), np.ascontiguousarray(b, np.float64).ravel())
+            for a, b in segments]
+    n = len(segs)
+    out = np.zeros((n, 2, 4), np.float64)
+    if n == 0:
+        return out
+    flat = np.concatenate([np.concatenate([a, b]) for a, b in segs]) if n else np.zeros(0)
+    ncomp = np.array([len(a) for a, _ in segs], np.uint32)
+    nreq = np.array([len(a) + len(b) for a, b in segs], np.uint32)
+    off = np.zeros(n, np.int64)
+    off[1:] = np.cumsum(nreq.astype(np.int64))[:-1]
+    flat = np.ascontiguousarray(flat if len(flat) else np.zeros(1), np.float64)
+    msg = C.create_string_buffer(1024)
+    opts = _opts(device)
+    rc = N.lib.cace_metrics_select(ptr(flat), ptr(off), ptr(ncomp), ptr(nreq), n, ptr(out), int(spec),
+                                   C.byref(opts), msg, len(msg))
+    if rc != N.CACE_OK:
+        _raise(rc, msg)
+    return out
+
+
 def run(trace: Trace, catalog: ModelCatalog, cluster: ClusterConfig = ClusterConfig(),
         policy: PolicyConfig = PolicyConfig(), device: int = 0, kernel: int = KERNEL_AUTO) -> SimulationReport:
     """``cacesim::run`` (engine.cpp:76-239) on the GPU: one scenario, full report."""

@@ -1085,6 +1085,36 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
   return rc;
 }
 
+int32_t cace_metrics_select(const double* samples, const int64_t* off, const uint32_t* ncomp,
+                            const uint32_t* nreq, int64_t n_segments, double* stat, int32_t spec,
+                            const cace_opts_t* opts, char* msg, size_t msg_cap) {
+  return guarded(msg, msg_cap, [&]() -> int32_t {
+    require_device(opts);
+    if (n_segments <= 0) return CACE_OK;
+    if (!samples || !off || !ncomp || !nreq || !stat) throw Invalid{CACE_E_INVALID, "cace: NULL argument"};
+    int64_t total = 0;
+    for (int64_t b = 0; b < n_segments; ++b) {
+      if (ncomp[b] > nreq[b] || off[b] < 0) throw Invalid{CACE_E_INVALID, "cace: bad segment"};
+      total = std::max<int64_t>(total, off[b] + (int64_t)nreq[b]);
+    }
+    cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
+    DBuf<double> d_samp, d_stat;
+    DBuf<int64_t> d_off;
+    DBuf<uint32_t> d_nc, d_nr;
+    d_samp.upload(samples, std::max<int64_t>(total, 1), s);
+    d_off.upload(off, n_segments, s);
+    d_nc.upload(ncomp, n_segments, s);
+    d_nr.upload(nreq, n_segments, s);
+    d_stat.alloc((size_t)n_segments * 8, s);
+    MetricsParams mp{d_samp.p, d_off.p, d_nc.p, d_nr.p, d_stat.p, spec};
+    metrics_select_kernel<<<(unsigned)(2 * n_segments), METRICS_BLOCK, 0, s>>>(mp);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(stat, d_stat.p, (size_t)n_segments * 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return CACE_OK;
+  });
+}
+
 // ---------------- trace ingestion (parse_trace / load_trace) --------------
 
 struct cace_trace_jsonl {

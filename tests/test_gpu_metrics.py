@@ -161,3 +161,49 @@ def test_average_metrics_matches_reference_formula():
     assert avg["cache_hit_rate"] == ((0.1 + 0.2) + 0.30000000000000004) / 3.0
     assert avg["evictions"] == 10.0 and avg["ttft_completion"]["count"] == 15
     assert avg["ttft_completion"]["p99_s"] == 2.0
+
+
+def _nearest_rank_stats(a):
+    """summarize's order statistics (metrics.cpp:14-33) on the sorted samples."""
+    if len(a) == 0:
+        return np.zeros(4)
+    s = np.sort(np.asarray(a, np.float64))
+    n = len(s)
+    out = []
+    for q in (0.50, 0.95, 0.99):
+        r = int(np.ceil(q * float(n)))
+        r = min(max(r, 1), n)
+        out.append(s[r - 1])
+    out.append(s[-1])
+    return np.array(out)
+
+
+@pytest.mark.parametrize("spec", [0, 1, 2])
+def test_metrics_select_kernel_edges(spec):
+    """The select kernel alone against np.sort + nearest rank, bit-exact:
+    lengths around the shared-list (5120), in-place (2 x 5120) and
+    speculation (16384) thresholds, heavy duplicates, constants, values
+    straddling the top-byte boundary at 2.0, zeros and subnormals."""
+    rng = np.random.default_rng(42 + spec)
+    lens = [1, 2, 3, 31, 5119, 5120, 5121, 10239, 10240, 10241, 16383, 16384, 16385, 70000]
+    segs = []
+    for k, n in enumerate(lens):
+        kind = k % 5
+        if kind == 0:
+            a = rng.exponential(3.0, n)
+        elif kind == 1:
+            a = np.round(rng.exponential(2.0, n), 2)  # heavy duplicates
+        elif kind == 2:
+            a = np.full(n, 1.25)
+        elif kind == 3:
+            a = rng.uniform(1.9, 2.1, n)  # top byte changes at 2.0
+        else:
+            a = np.concatenate([np.zeros(n // 2), rng.uniform(0, 1e-310, n - n // 2)])
+        b = rng.permutation(a)[: max(1, n // 3)] * 1.5
+        segs.append((a, b))
+    segs.append((np.zeros(0), rng.uniform(0, 5, 20000)))  # empty class -> zeros
+    got = P.metrics_select(segs, spec=spec)
+    for i, (a, b) in enumerate(segs):
+        for c, x in enumerate((a, b)):
+            want = _nearest_rank_stats(x)
+            assert np.array_equal(bits(got[i, c]), bits(want)), (i, c, len(x), got[i, c], want)
