@@ -470,21 +470,21 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C, int MW, bool DUMP, int MINB>
+template <int C, int MW, int DM, int MINB>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DUMP, MINB>,
+    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DM, MINB>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
-  replay_lane_kernel<C, MW, DUMP, MINB><<<grid, LANE_BLOCK, smem, s>>>(P);
+  replay_lane_kernel<C, MW, DM, MINB><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 
-template <int MW, bool DUMP, int MINB = CACE_LANE_MIN_BLOCKS>
+template <int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS>
 void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
   switch (C) {
 #define CASE(k) \
-  case k: launch_lane<k, MW, DUMP, MINB>(P, count, smem, s); break;
+  case k: launch_lane<k, MW, DM, MINB>(P, count, smem, s); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
@@ -511,17 +511,18 @@ void dispatch_warp(bool dump, int spl, const ReplayParams& P, int64_t count, cud
     dump ? launch_warp<2, true>(P, count, s) : launch_warp<2, false>(P, count, s);
 }
 
-void dispatch_lane(bool dump, int C, const ReplayParams& P, int64_t count, size_t smem,
-                   cudaStream_t s, bool latency) {
+void dispatch_lane(int dm, int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s,
+                   bool latency) {
   const bool mw1 = P.cat.M <= 32;
-  if (latency && !dump && mw1) {
-    dispatch_lane_c<1, false, kLaneLatencyMinBlocks>(C, P, count, smem, s);
+  if (latency && dm == 0 && mw1) {
+    dispatch_lane_c<1, 0, kLaneLatencyMinBlocks>(C, P, count, smem, s);
     return;
   }
-  if (dump)
-    mw1 ? dispatch_lane_c<1, true>(C, P, count, smem, s) : dispatch_lane_c<2, true>(C, P, count, smem, s);
-  else
-    mw1 ? dispatch_lane_c<1, false>(C, P, count, smem, s) : dispatch_lane_c<2, false>(C, P, count, smem, s);
+  switch (dm) {
+    case 0: mw1 ? dispatch_lane_c<1, 0>(C, P, count, smem, s) : dispatch_lane_c<2, 0>(C, P, count, smem, s); break;
+    case 1: mw1 ? dispatch_lane_c<1, 1>(C, P, count, smem, s) : dispatch_lane_c<2, 1>(C, P, count, smem, s); break;
+    default: mw1 ? dispatch_lane_c<1, 2>(C, P, count, smem, s) : dispatch_lane_c<2, 2>(C, P, count, smem, s); break;
+  }
 }
 
 ReplayParams replay_params(const cace_engine* e, const cace_scenario_t* d_sc, cace_summary_t* d_out,
@@ -549,10 +550,12 @@ void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams 
   P.seg_begin = b;
   P.seg_end = end;
   const bool dump_on = P.dump.slot != nullptr;
+  // samples set = the RunMetrics pipeline, which dumps nothing else
+  const int dm = !dump_on ? 0 : (P.dump.samples ? 2 : 1);
   if (g.warp)
     dispatch_warp(dump_on, g.C, P, end - b, ws);
   else
-    dispatch_lane(dump_on, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, latency);
+    dispatch_lane(dm, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, latency);
 }
 
 void fill_status(cace_engine* e, cace_summary_t* d_out, cudaStream_t s) {

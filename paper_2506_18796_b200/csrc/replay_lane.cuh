@@ -353,7 +353,7 @@ __device__ __forceinline__ void flush_samples(const double* tile, double* mine, 
 // shared-memory shadows (fewer live registers: best for the 16-warp
 // instantiations) or unrolled over the slot registers (best when registers
 // are plentiful, the 12-warp instantiations).
-template <int C, int MW, bool DUMP, bool XR = true>
+template <int C, int MW, int DM, bool XR = true>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
                                 const CatShared& K, const LaneSmem& S) {
   const cace_scenario_t sc = P.scen[sidx];
@@ -402,14 +402,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   bool dump_outcomes = false;
   double* samples = nullptr;  // this scenario's metrics samples
   uint32_t ncomp_t = 0;
-  if (DUMP && !shadow) {
+  if (DM != 0 && !shadow) {
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
-    dump_outcomes = P.dump.cold || P.dump.queue_wait || P.dump.load_wait || P.dump.prefill ||
-                    P.dump.decode || P.dump.ttft || P.dump.e2e;
+    if (DM == 1)
+      dump_outcomes = P.dump.cold || P.dump.queue_wait || P.dump.load_wait || P.dump.prefill ||
+                      P.dump.decode || P.dump.ttft || P.dump.e2e;
     if (dslot >= 0 && P.dump.samples) samples = P.dump.samples + doff;
   }
-  if (DUMP) ncomp_t = P.trace_ncomp[sc.trace];  // shadows too: the sample tile flush is collective
+  if (DM != 0) ncomp_t = P.trace_ncomp[sc.trace];  // shadows too: the sample tile flush is collective
   RecStream rs;
   rs.init(tr, n, S.rec);
   Window<MW> win;
@@ -666,7 +667,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         const int vm = slot_model(S.word[v * st]);
         S.slot_of[vm * st] = 0;
         he = hmix(he, dbits(cur.t) ^ ((uint64_t)vm << 32));
-        if (DUMP && dslot >= 0) {
+        if (DM == 1 && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
             if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = cur.t;
@@ -711,7 +712,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       me2e = e2e > me2e ? e2e : me2e;
     }
     ho = hmix(ho, dbits(ttft) ^ (hit ? 0ull : 1ull));
-    if (DUMP && dslot >= 0) {
+    if (DM == 1 && dslot >= 0) {
       if (dump_outcomes) {  // per-request outcomes in the caller's request order
         const int64_t o = doff + P.perm[base + k];
         if (P.dump.cold) P.dump.cold[o] = hit ? 0 : 1;
@@ -726,7 +727,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     // metrics samples (compute_run_metrics, metrics.cpp:44-52): TTFT of
     // completion requests, then E2E of reasoning requests
 #ifndef CACE_HOST_EMULATION
-    if (DUMP && P.dump.samples) {  // warp-collective (shadow lanes take part, write nothing)
+    if (DM == 2 || (DM == 1 && P.dump.samples)) {  // warp-collective (shadow lanes take part, write nothing)
       const bool comp = (mc >> 16) == CACE_COMPLETION;
       const uint32_t ci = R.ci;
       double* tc = S.samp + (comp ? 0 : kSampT * 32);
@@ -738,7 +739,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       }
     }
 #else
-    if (DUMP && samples) {
+    if (DM != 0 && samples) {
       const bool comp = (mc >> 16) == CACE_COMPLETION;
       samples[comp ? R.ci : ncomp_t + R.ci] = comp ? ttft : e2e;
     }
@@ -751,7 +752,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   }
 
 #ifndef CACE_HOST_EMULATION
-  if (DUMP && P.dump.samples) {  // partial tiles
+  if (DM == 2 || (DM == 1 && P.dump.samples)) {  // partial tiles
     const uint32_t nco = ncomp_t, nre = n - ncomp_t;
     __syncwarp();
     if (nco % kSampT) flush_samples(S.samp, samples, nco - nco % kSampT, nco % kSampT);
@@ -777,7 +778,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   o.eviction_hash = he;
   o.outcome_hash = ho;
   P.out[sidx] = o;
-  if (DUMP && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
+  if (DM == 1 && dslot >= 0 && P.dump.n_evict) P.dump.n_evict[dslot] = dn_ev;
 }
 
 constexpr uint64_t kShadowBit = 1ull << 62;  // plan entry = warp padding lane
@@ -811,7 +812,10 @@ inline size_t lane_smem_bytes(int M, int C, bool dump) {
 // chain length bounds the step (capi.cu picks).
 constexpr int kLaneLatencyMinBlocks = 3;
 
-template <int C, int MW, bool DUMP, int MINB = CACE_LANE_MIN_BLOCKS>
+// DM: 0 summary only; 1 full dump (outcomes, eviction log, samples) for the
+// scenarios with a dump slot; 2 metrics samples only (the RunMetrics
+// pipeline: no outcome / eviction-log code or registers).
+template <int C, int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS>
 __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = P.cat.M;
@@ -831,7 +835,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_word + (size_t)C * LANE_BLOCK);  // [M][LANE_BLOCK]
   unsigned char* wbase =
       smem + ((((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
-      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DUMP);
+      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
   ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
   WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
   double* w_samp = reinterpret_cast<double*>(w_win + M);
@@ -858,7 +862,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x, l_prm + threadIdx.x,
                    l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win, w_samp};
-  replay_scenario<C, MW, DUMP, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
+  replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
 }
 #endif  // CACE_HOST_EMULATION
 
