@@ -334,14 +334,22 @@ constexpr int kSampT = 4;
 
 #ifndef CACE_HOST_EMULATION
 // Warp-collective: lane q's tile column [0, cnt) -> mine(q)[base + 0 .. cnt).
-__device__ __forceinline__ void flush_samples(const double* tile, double* mine, int64_t base, int cnt) {
+// The warp's 32 destination pointers (null: write nothing) and the trace's
+// completion count sit after the tile, so they hold no registers.
+__device__ __forceinline__ double* const* samp_ptrs(double* tile) {
+  return reinterpret_cast<double* const*>(tile + 2 * kSampT * 32);
+}
+__device__ __forceinline__ uint32_t samp_ncomp(double* tile) {
+  return *reinterpret_cast<const uint32_t*>(tile + 2 * kSampT * 32 + 32);
+}
+__device__ __forceinline__ void flush_samples(const double* tile, double* const* ptrs, int64_t base, int cnt) {
   const int lane = threadIdx.x & 31;
   const int j = lane % kSampT;
 #pragma unroll
   for (int i = 0; i < kSampT; ++i) {
     const int q = lane / kSampT + (32 / kSampT) * i;
     const double v = tile[j * 32 + q];
-    double* pq = reinterpret_cast<double*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), q));
+    double* pq = ptrs[q];
     if (pq && j < cnt) pq[base + j] = v;
   }
 }
@@ -410,7 +418,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                       P.dump.decode || P.dump.ttft || P.dump.e2e;
     if (dslot >= 0 && P.dump.samples) samples = P.dump.samples + doff;
   }
-  if (DM != 0) ncomp_t = P.trace_ncomp[sc.trace];  // shadows too: the sample tile flush is collective
+  if (DM != 0) ncomp_t = P.trace_ncomp[sc.trace];
+#ifndef CACE_HOST_EMULATION
+  if (DM == 2 || (DM == 1 && P.dump.samples)) {  // the sample tile's pointer table (shadows too: flushes are collective)
+    reinterpret_cast<double**>(S.samp + 2 * kSampT * 32)[threadIdx.x & 31] = samples;
+    if ((threadIdx.x & 31) == 0) *reinterpret_cast<uint32_t*>(S.samp + 2 * kSampT * 32 + 32) = ncomp_t;
+    __syncwarp();
+  }
+#endif
   RecStream rs;
   rs.init(tr, n, S.rec);
   Window<MW> win;
@@ -734,7 +749,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       tc[(ci % kSampT) * 32 + (threadIdx.x & 31)] = comp ? ttft : e2e;
       if (ci % kSampT == kSampT - 1) {
         __syncwarp();
-        flush_samples(tc, samples, (int64_t)(comp ? 0 : ncomp_t) + ci - (kSampT - 1), kSampT);
+        flush_samples(tc, samp_ptrs(S.samp), (int64_t)(comp ? 0 : samp_ncomp(S.samp)) + ci - (kSampT - 1), kSampT);
         __syncwarp();
       }
     }
@@ -753,11 +768,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
 
 #ifndef CACE_HOST_EMULATION
   if (DM == 2 || (DM == 1 && P.dump.samples)) {  // partial tiles
-    const uint32_t nco = ncomp_t, nre = n - ncomp_t;
+    const uint32_t nco = samp_ncomp(S.samp), nre = n - nco;
     __syncwarp();
-    if (nco % kSampT) flush_samples(S.samp, samples, nco - nco % kSampT, nco % kSampT);
+    if (nco % kSampT) flush_samples(S.samp, samp_ptrs(S.samp), nco - nco % kSampT, nco % kSampT);
     if (nre % kSampT)
-      flush_samples(S.samp + kSampT * 32, samples, (int64_t)ncomp_t + nre - nre % kSampT, nre % kSampT);
+      flush_samples(S.samp + kSampT * 32, samp_ptrs(S.samp), (int64_t)nco + nre - nre % kSampT, nre % kSampT);
   }
 #endif
   if (shadow) return;
@@ -798,7 +813,7 @@ inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
   return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + 4 * 4 + C * 8 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M, bool dump) {
-  return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? 2 * kSampT * 32 * sizeof(double) : 0);
+  return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? (2 * kSampT * 32 + 32 + 2) * sizeof(double) : 0);  // 16-B multiple: keeps the next warp's records aligned
 }
 inline size_t lane_smem_bytes(int M, int C, bool dump) {
   const size_t a = (((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
