@@ -40,8 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
-                    help="BASELINE config: 4 = 1M scenarios x 100k (default), 5 = 256-model pool, 10M bursty")
+    ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5],
+                    help="BASELINE config: 4 = 1M scenarios x 100k (default), 3 = 4096 weight vectors x 100k, "
+                         "2 = CACE vs LRU on one 10k trace, 5 = 256-model pool, 10M bursty")
+    ap.add_argument("--capacity", type=int, default=3, help="cfg2/cfg3 capacity (memory budget fits 3)")
     ap.add_argument("--requests", type=int, default=None, help="requests per trace (cfg4 100k, cfg5 10M)")
     ap.add_argument("--seeds", type=int, default=32)
     ap.add_argument("--scenarios", type=int, default=8192, help="cfg5 scenario count")
@@ -66,11 +68,25 @@ def workload(args, part: int = 0):
 
     if args.config == 5:
         return synth.config5(n_requests=args.requests, n_scenarios=args.scenarios, trace_seed=1 + part)
+    if args.config == 3:
+        return synth.config3(n_requests=args.requests, capacity=args.capacity, seed=1 + part)
+    if args.config == 2:
+        return synth.config2(n_requests=args.requests, seed=1 + part, capacity=args.capacity)
     catalog = synth.eight_model_catalog()
     traces = [synth.mixed_trace(catalog, args.requests, seed=1 + part * args.seeds + s) for s in range(args.seeds)]
     pols = synth.weight_vectors_cfg3()[:: args.vectors_stride]
     sc = synth.scenario_grid(pols, range(1, 9), args.seeds, catalog.max_expected_output_tokens())
     return catalog, traces, sc
+
+
+def workload_name(args, S, n):
+    if args.config == 4:
+        return "BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests" % (args.seeds, n)
+    if args.config == 3:
+        return "BASELINE config 3: 4096 weight vectors x one %d-request trace, capacity %d" % (n, args.capacity)
+    if args.config == 2:
+        return "BASELINE config 2: CACE and LRU on one %d-request trace, capacity %d" % (n, args.capacity)
+    return "BASELINE config 5: %d scenarios x %d-request bursty trace, 256 CodeLLMs, capacity 32, window 1024" % (S, n)
 
 
 class ClockSampler:
@@ -190,7 +206,7 @@ def run_reference_arm(args):
 def main():
     args = parse()
     if args.requests is None:
-        args.requests = 10_000_000 if args.config == 5 else 100_000
+        args.requests = {2: 10_000, 5: 10_000_000}.get(args.config, 100_000)
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -370,10 +386,7 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": ("BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests"
-                                % (args.seeds, n_req)) if args.config == 4 else
-                               ("BASELINE config 5: %d scenarios x %d-request bursty trace, 256 CodeLLMs, capacity 32, "
-                                "window 1024" % (S_total, n_req)),
+        "config": {"workload": workload_name(args, S_total, n_req),
                    "scenarios": S_total, "requests_per_trace": n_req, "models": len(catalog),
                    "parallelism": (f"scenario shards x{world}, each rank its own full sweep (weak)"
                                    if args.scaling == "weak" else f"one sweep split over {world} ranks (strong)"),

@@ -337,9 +337,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->segs.clear();
   e->bad_idx.clear();
   e->bad_code.clear();
-  auto capof = [&](int64_t i) {
-    return (int)((int64_t)sc[i].num_accelerators * sc[i].models_per_accelerator);
-  };
+  auto capof = [&](int64_t i) { return (int)effective_capacity(sc[i], e->cat.M); };
   // Kernel choice: lane-per-scenario for capacities <= 16 and pools <= 64
   // models (register-resident slots and window); warp-per-scenario otherwise
   // (BASELINE config 5 regime) or when forced with CACE_KERNEL_WARP.

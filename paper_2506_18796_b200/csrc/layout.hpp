@@ -94,6 +94,7 @@ struct DefaultInitAlloc : std::allocator<T> {
 // Replay-order layout of all traces, concatenated.
 struct HostLayout {
   int T = 0;
+  int M = 0;                       // catalog size the layout was built for
   std::vector<int64_t> off;        // [T+1]
   std::vector<ReqRec, DefaultInitAlloc<ReqRec>> rec;  // [N] sorted by (arrival, index)
   ReqRec* ext_rec = nullptr;  // if set (>= N records): records are written here instead of `rec`
@@ -115,10 +116,13 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
   const int M = cat.M;
   if (n_traces < 0 || (n_traces > 0 && !traces)) throw Invalid{CACE_E_INVALID, "cace: bad traces"};
   L.T = n_traces;
+  L.M = M;
   L.off.assign(n_traces + 1, 0);
   for (int t = 0; t < n_traces; ++t) {
-    if (traces[t].n_requests < 0 || traces[t].n_requests > 0xfffffff0LL)
-      throw Invalid{CACE_E_INVALID, "cace: trace too long"};
+    // replay index k < 2^30: the kernels pack (event kind, push seq) into one
+    // 32-bit cursor word (replay_lane.cuh)
+    if (traces[t].n_requests < 0 || traces[t].n_requests >= (1LL << 30))
+      throw Invalid{CACE_E_INVALID, "cace: trace too long (more than 2^30 - 1 requests)"};
     L.off[t + 1] = L.off[t] + traces[t].n_requests;
   }
   const int64_t N = L.off[n_traces];
@@ -237,6 +241,16 @@ inline void build_layout(const HostCatalog& cat, const cace_trace_t* traces, int
     throw Invalid{CACE_E_INVALID, "cace: load/service times too large (event clock would exceed 1e28 s)"};
 }
 
+// Slots a replay can ever use: capacity = num_accelerators x
+// models_per_accelerator (engine.cpp:83-84), clamped to the pool size M.  With
+// capacity >= M a non-resident head always finds a free slot (at most M - 1
+// other models are resident), so nothing is ever evicted and the replay -- every
+// outcome, counter and max_resident -- is identical to capacity = M.
+inline int64_t effective_capacity(const cace_scenario_t& sc, int M) {
+  const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
+  return cap < (int64_t)M ? cap : (int64_t)M;
+}
+
 // Reference run() preconditions (engine.cpp:79-92, 17-20) for one scenario:
 // the SimError it would raise (code | model << 8), CACE_OK, or CACE_E_INVALID
 // for inputs outside the engine's domain.
@@ -254,7 +268,7 @@ inline int32_t precheck(const HostLayout& L, const cace_scenario_t& sc) {
   if (L.bad_model[sc.trace] >= 0) return CACE_E_RATES | (L.bad_model[sc.trace] << 8);
   const int64_t cap = (int64_t)sc.num_accelerators * sc.models_per_accelerator;
   if (cap < 1) return CACE_E_DEADLOCK;  // nothing can ever load (engine.cpp:235-237)
-  if (cap > kMaxWarpC) return CACE_E_INVALID | (2 << 8);
+  if (effective_capacity(sc, L.M) > kMaxWarpC) return CACE_E_INVALID | (2 << 8);
   return CACE_OK;
 }
 

@@ -86,23 +86,7 @@ __device__ __forceinline__ void load_rec(const ReqRec* p, double& a, double& pf,
 // Slot word: model (bits 0-15) | lex rank of model_id (bits 18-31).
 __device__ __forceinline__ int slot_model(int v) { return v & 0xffff; }
 __device__ __forceinline__ int slot_lex(int v) { return (int)((unsigned)v >> 18); }
-__device__ __forceinline__ bool is_idle(double st) { return __double2hiint(st) >= 0; }
-
-// Number of Busy slots (sign bits), summed as a balanced tree so the count
-// is not a C-deep dependency chain.
-template <int C>
-__device__ __forceinline__ int busy_count(const double (&st)[C]) {
-  int b[C];
-#pragma unroll
-  for (int s = 0; s < C; ++s) b[s] = (int)((unsigned)__double2hiint(st[s]) >> 31);
-#pragma unroll
-  for (int w = 1; w < C; w *= 2)
-#pragma unroll
-    for (int s = 0; s + w < C; s += 2 * w) b[s] += b[s + w];
-  return b[0];
-}
-
-// Event key (time, kind, seq) of engine.cpp:49-55.
+// Event key (time, kind, seq) of engine.cpp:49-55 (warp kernel).
 struct Cursor {
   double t;
   int kind;
@@ -136,7 +120,12 @@ __device__ __forceinline__ float fast_rcp(float x) {
 // Exact fp64 P1 of eviction_score (policy.cpp:50-53) with the glibc log.
 // Out of line: one copy serves every unrolled candidate of the rare exact
 // path, and its temporaries do not add to the replay loop's register peak.
-__device__ __noinline__ double exact_p1(double now, double last_used, bool verbatim, int log_variant,
+#ifdef CACE_EXACT_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+double exact_p1(double now, double last_used, bool verbatim, int log_variant,
                                         const double* tab, const double* tab2) {
   const double d = now - last_used;
   const double t = d < 1.0 ? 1.0 : d;  // std::max(d, 1.0)
@@ -309,21 +298,38 @@ struct CatShared {
   const int* lex;     // rank of model_id under std::string <
 };
 
+// One resident slot: completion time of its last service (= last_used_s once
+// that ServiceComplete has popped), the service's push seq, and the slot word
+// (model | lex rank << 18).  16 B: one 128-bit shared load per slot.
+struct alignas(16) SlotEnt {
+  double done;
+  uint32_t seq;
+  int word;
+};
+
 // Per-lane shared-memory columns (element i at [i * stride]) and the lane's
 // warp-shared tables.
 struct LaneSmem {
   float* p4f;        // [M] p2 + p4 = p2 + w1 * (tokens / normalizer), fp32 (screening)
   double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67)
-  double* done;      // [C] |stime|: completion time of the slot's last service
+  SlotEnt* slot;     // [C] resident slots
   float* prm;        // [4] screen constants: 1/w, p1 scale, p1 offset, margin (+inf: no screen)
-  uint32_t* seq;     // [C] ServiceComplete push seq of each busy slot
-  int* word;         // [C] slot word: model | lex rank << 18
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
   int stride;
   ReqRec* rec;       // warp: record double buffer [64]
   WinEnt* win;       // warp: window table [M]
   double* samp;      // warp: metrics sample tile [2 classes][kSampT][32 lanes] (DUMP only)
 };
+
+// Event cursor (time, kind, seq) of engine.cpp:49-55 as (ct, cw) with
+// cw = kind << 30 | seq (replay indices are < 2^30, layout.hpp).  A slot's
+// ServiceComplete (done, 1, seq) has popped -- the slot is Idle with
+// last_used_s = done -- iff its key is <= the cursor.
+constexpr uint32_t kKindSC = 1u << 30;
+constexpr uint32_t kKindArr = 2u << 30;
+__device__ __forceinline__ bool sc_popped(double done, uint32_t seq, double ct, uint32_t cw) {
+  return done < ct || (done == ct && (kKindSC | seq) <= cw);
+}
 
 // Metrics samples leave through a per-warp shared tile: the lanes of a warp
 // replay the same trace in lockstep, so request k has the same class-local
@@ -357,10 +363,9 @@ __device__ __forceinline__ void flush_samples(const double* tile, double* const*
 
 // Replays one scenario (see the file comment).  shadow lanes (warp padding)
 // replay a copy of a real scenario for lockstep and write nothing.
-// XR: the exact fallback as rolled loops over the idle slots reading the
-// shared-memory shadows (fewer live registers: best for the 16-warp
-// instantiations) or unrolled over the slot registers (best when registers
-// are plentiful, the 12-warp instantiations).
+// XR: the exact fallback as rolled loops over the idle slots re-reading the
+// shared slot table (compact code, few live registers) or unrolled over the
+// slot entries already in registers.
 template <int C, int MW, int DM, bool XR = true>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
                                 const CatShared& K, const LaneSmem& S) {
@@ -375,8 +380,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const bool verbatim = sc.p1_mode == CACE_P1_VERBATIM;
   const uint32_t w = (uint32_t)sc.window_length;
   const double norm = (double)sc.output_token_normalizer;
-
-  // fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0
 
   const int st = S.stride;
   // fp32 screening is valid while every p2 + p4 is finite and moderate; the
@@ -400,8 +403,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   }
   // screen constants live in shared memory: read only by deciding lanes, so
   // they hold no registers across the replay loop
+  // (fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0)
   S.prm[0] = 1.0f / (float)sc.window_length;
-  S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);  // p1 = p1s * p1v + p1o
+  S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
   S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
   S.prm[3 * st] = screen_ok ? 6e-5f + 1e-6f * (tbound + 4.0f) : INFINITY;
 
@@ -431,16 +435,15 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   Window<MW> win;
   if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M, tr, n, S.win);
 
-  // Slots (registers), sign-encoded (file comment); the push seq (tie-break
-  // of equal completion times) lives in shared memory.
-  double stime[C];
-#pragma unroll
-  for (int s = 0; s < C; ++s) {
-    S.word[s * st] = 0xffff;
-    stime[s] = 0.0;
-  }
+  // Slots [0, occ) are resident (shared slot table); there is no eager
+  // per-slot state machine: a slot is Busy until its ServiceComplete key
+  // passes the cursor (sc_popped), and then Idle with last_used_s = done
+  // (a completion sets last_used to its own event time, engine.cpp:219-230;
+  // the only Loading slot is the head's own, which is served the moment its
+  // LoadComplete pops).
   int occ = 0;
-  Cursor cur{-INFINITY, 2, 0};
+  double ct = -INFINITY;  // cursor time
+  uint32_t cw = kKindArr;  // cursor kind << 30 | seq
 
   // loads == misses == n - hits; evictions == loads - final occupancy.
   uint32_t hits = 0;
@@ -458,51 +461,26 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const uint32_t mc = R.mc;
     const int m = (int)(mc & 0xffffu);
 
-    // Head not yet pending: advance to its Arrival; completions with a
-    // smaller key (done <= a) idle their slots (engine.cpp:219-230).
-    if (!(a < cur.t)) {
-      const double na = -a;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (stime[s] >= na) stime[s] = fabs(stime[s]);
-      cur = Cursor{a, 2, k};
+    // Head not yet pending: the next relevant event is its Arrival (a, 2, k);
+    // completions with a smaller key only idle their slots (engine.cpp:219-230).
+    if (!(a < ct)) {
+      ct = a;
+      cw = kKindArr | k;
     }
 
     // classify (engine.cpp:163-173): resident (never Loading here) -> hit
     int hs = (int)S.slot_of[m * st] - 1;
-    const int nbusy = busy_count<C>(stime);
-    const bool decide = hs < 0 && occ == C && C - nbusy >= 2;
-
     double lw = 0.0;
     const bool hit = hs >= 0;
     if (hit) {
       ++hits;
-      // Busy iff its ServiceComplete key (td, 1, tq) is after the cursor
-      // (the sign of stime[hs] says the same; the shadow avoids a dynamic
-      // register read).
-      const double td = S.done[hs * st];
-      const uint32_t tq = S.seq[hs * st];
-      // predicates evaluated side by side (no short-circuit chain behind the loads)
-      const bool tie_busy = (cur.kind == 0) | ((cur.kind == 1) & (tq > cur.seq));
-      if ((td > cur.t) | ((td == cur.t) & tie_busy)) {
-        // Busy: blocked until the model's own ServiceComplete (td, 1, tq).
-        // Completions with key <= it become Idle: done < td, and equal
-        // times break ties on the push seq.
-        cur = Cursor{td, 1, tq};
-        const double ntd = -td;
-        int neq = 0;  // slots completing exactly at td, hs included
-#pragma unroll
-        for (int s = 0; s < C; ++s) {
-          if (stime[s] > ntd) stime[s] = fabs(stime[s]);
-          neq += stime[s] == ntd ? 1 : 0;
-        }
-        if (neq > 1) {
-          // equal completion times pop in push order: earlier seq -> Idle
-          // (hs itself has seq == tq and is overwritten by the service below)
-#pragma unroll
-          for (int s = 0; s < C; ++s)
-            if (stime[s] == ntd && S.seq[s * st] < tq) stime[s] = fabs(stime[s]);
-        }
+      // Busy: blocked until the model's own ServiceComplete (td, 1, tq)
+      // (engine.cpp:175-181); every earlier completion just idles its slot.
+      const double td = S.slot[hs * st].done;
+      const uint32_t tq = S.slot[hs * st].seq;
+      if (!sc_popped(td, tq, ct, cw)) {
+        ct = td;
+        cw = kKindSC | tq;
       }
     } else {
       int v;
@@ -510,50 +488,62 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
       } else {
-        if (nbusy == C) {
-          // every resident busy: the next event is the min-key
-          // ServiceComplete, whose slot is then the only Idle one.
+        // Full: the Idle residents are the eviction candidates
+        // (engine.cpp:189-208, policy.cpp:85-89).
+        double sd[C];
+        uint32_t sq[C];
+        int sw[C];
+        unsigned idm = 0;
+#pragma unroll
+        for (int s = 0; s < C; ++s) {
+          const SlotEnt e = S.slot[s * st];
+          sd[s] = e.done;
+          sq[s] = e.seq;
+          sw[s] = e.word;
+          idm |= sc_popped(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
+        }
+        if (idm == 0) {
+          // every resident busy: nothing to evict now (select_victim ->
+          // nullopt); the next event is the min-key ServiceComplete, whose
+          // slot is then the only Idle one (forced victim).
           int s1 = 0;
-          double t1 = stime[0];  // = -done: max t1 = min done
+          double t1 = sd[0];
+          uint32_t q1 = sq[0];
 #pragma unroll
           for (int s = 1; s < C; ++s)
-            if (stime[s] > t1 || (stime[s] == t1 && S.seq[s * st] < S.seq[s1 * st])) {
+            if (sd[s] < t1 || (sd[s] == t1 && sq[s] < q1)) {
               s1 = s;
-              t1 = stime[s];
+              t1 = sd[s];
+              q1 = sq[s];
             }
-          cur = Cursor{-t1, 1, S.seq[s1 * st]};
+          ct = t1;
+          cw = kKindSC | q1;
           v = s1;
-        } else if (!decide) {
-          v = 0;  // exactly one candidate
-#pragma unroll
-          for (int s = 1; s < C; ++s)
-            if (is_idle(stime[s])) v = s;
+        } else if ((idm & (idm - 1u)) == 0) {
+          v = __ffs(idm) - 1;  // exactly one candidate
         } else {
           // ---- eviction decision among >= 2 idle residents ----------
-          const double now = cur.t;
-          // Sorted-first = min (last_used, lex) over idle: the LRU victim,
-          // and the NaN rule of the exact CACE path.
-          auto sorted_first = [&]() {
+          const double now = ct;
+          if (is_lru) {
+            // sorted-first = min (last_used, lex) over idle (policy.cpp:92-100)
             int f = -1;
             double flu = 0.0;
             int flex = 0;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              const int lx = slot_lex(S.word[s * st]);
-              if (is_idle(stime[s]) && (f < 0 || stime[s] < flu || (stime[s] == flu && lx < flex))) {
-                f = s;
-                flu = stime[s];
-                flex = lx;
-              }
+              const int lx = slot_lex(sw[s]);
+              if ((idm >> s) & 1u)
+                if (f < 0 || sd[s] < flu || (sd[s] == flu && lx < flex)) {
+                  f = s;
+                  flu = sd[s];
+                  flex = lx;
+                }
             }
-            return f;
-          };
-          // p3 (policy.cpp:57-64): rank / w when the model's first pending
-          // request lies in the window [k, min(k + w, arrived)), else 1.
-          // Idle residents are not the head's model, so first > k.
-          if (is_lru) {
-            v = sorted_first();
+            v = f;
           } else {
+            // p3 (policy.cpp:57-64): rank / w when the model's first pending
+            // request lies in the window [k, min(k + w, arrived)), else 1.
+            // Idle residents are not the head's model, so first > k.
             // fp32 screening with a rigorous bound: if one candidate's
             // approximate total beats every other by more than the bound it
             // is the exact arg-max.  |dL| <= 2.3e-5 (lg2.approx, ln t < 70)
@@ -567,8 +557,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              const int ms = slot_model(S.word[s * st]);
-              const float t = fmaxf((float)(now - stime[s]), 1.0f);  // max(d, 1) in fp32
+              const int ms = slot_model(sw[s]);
+              const float t = fmaxf((float)(now - sd[s]), 1.0f);  // max(d, 1) in fp32
               const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
               const float p1 = fmaf(p1s, p1v, p1o);
               float p3 = 0.0f;
@@ -577,7 +567,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
               }
               float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
-              T = is_idle(stime[s]) ? T : -INFINITY;
+              T = ((idm >> s) & 1u) ? T : -INFINITY;
               bs = T > best ? s : bs;
               second = fmaxf(second, fminf(best, T));
               best = fmaxf(best, T);
@@ -591,37 +581,20 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               // One pass: the best non-NaN total, ties to the earlier entry in
               // (last_used, lex) order; a NaN sorted-first entry keeps the
               // slot (no later total compares greater than NaN).
-              if constexpr (XR) {
-              // Rolled loops over the idle slots, reading last_used from the
-              // shared completion-time shadow (equal to |stime| once Idle):
-              // compact code and few live registers for this rare path.
-              unsigned idm = 0;
-#pragma unroll
-              for (int s = 0; s < C; ++s) idm |= is_idle(stime[s]) ? (1u << s) : 0u;
               int f = -1;
               double flu = 0.0;
               int flex = 0;
-#pragma unroll 1
-              for (unsigned q = idm; q; q &= q - 1u) {  // sorted-first: min (last_used, lex)
-                const int s = __ffs(q) - 1;
-                const double lu = S.done[s * st];
-                const int lx = slot_lex(S.word[s * st]);
-                if (f < 0 || lu < flu || (lu == flu && lx < flex)) {
+              bool f_nan = false;
+              double bt = 0.0, blu = 0.0;
+              int blex = 0, bv = -1;
+              auto cand = [&](int s, double lu, int wd) {
+                const int ms = slot_model(wd);
+                const int lx = slot_lex(wd);
+                if (f < 0 || lu < flu || (lu == flu && lx < flex)) {  // sorted-first so far
                   f = s;
                   flu = lu;
                   flex = lx;
                 }
-              }
-              bool f_nan = false;
-              double bt = 0.0, blu = 0.0;
-              int blex = 0, bv = -1;
-#pragma unroll 1
-              for (unsigned q = idm; q; q &= q - 1u) {
-                const int s = __ffs(q) - 1;
-                const double lu = S.done[s * st];
-                const int wd = S.word[s * st];
-                const int ms = slot_model(wd);
-                const int lx = slot_lex(wd);
                 const double p1 = variant == CACE_MINUS_P1
                                       ? 0.0
                                       : exact_p1(now, lu, verbatim, P.log_variant, P.log_tab, P.log_tab2);
@@ -633,92 +606,67 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 }
                 const double p4 = S.p4d[ms * st];
                 const double T = ((p1 + p2) + p3) + p4;
-                if (s == f) f_nan = T != T;
                 if (T == T && (bv < 0 || T > bt || (T == bt && (lu < blu || (lu == blu && lx < blex))))) {
                   bt = T;
                   blu = lu;
                   blex = lx;
                   bv = s;
                 }
-              }
-              v = f_nan ? f : bv;
+                return T != T;
+              };
+              unsigned nanm = 0;
+              if constexpr (XR) {
+#pragma unroll 1
+                for (unsigned q = idm; q; q &= q - 1u) {
+                  const int s = __ffs(q) - 1;
+                  if (cand(s, S.slot[s * st].done, S.slot[s * st].word)) nanm |= 1u << s;
+                }
               } else {
-              const int f = sorted_first();
-              bool f_nan = false;
-              double bt = 0.0, blu = 0.0;
-              int blex = 0, bv = -1;
 #pragma unroll
-              for (int s = 0; s < C; ++s) {
-                if (!is_idle(stime[s])) continue;
-                const int wd = S.word[s * st];
-                const int ms = slot_model(wd);
-                const int lx = slot_lex(wd);
-                const double p1 = variant == CACE_MINUS_P1
-                                      ? 0.0
-                                      : exact_p1(now, stime[s], verbatim, P.log_variant, P.log_tab, P.log_tab2);
-                const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
-                double p3 = 0.0;
-                if (variant != CACE_MINUS_P3) {
-                  const WinEnt e = win.gather(ms);
-                  p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
-                }
-                const double p4 = S.p4d[ms * st];
-                const double T = ((p1 + p2) + p3) + p4;
-                if (s == f) f_nan = T != T;
-                if (T == T && (bv < 0 || T > bt ||
-                               (T == bt && (stime[s] < blu || (stime[s] == blu && lx < blex))))) {
-                  bt = T;
-                  blu = stime[s];
-                  blex = lx;
-                  bv = s;
-                }
+                for (int s = 0; s < C; ++s)
+                  if ((idm >> s) & 1u)
+                    if (cand(s, sd[s], sw[s])) nanm |= 1u << s;
               }
+              f_nan = (nanm >> f) & 1u;
               v = f_nan ? f : bv;
-              }
             }
           }
         }
         // residents.erase(victim); evictions++ (engine.cpp:205-206)
-        const int vm = slot_model(S.word[v * st]);
+        const int vm = slot_model(S.slot[v * st].word);
         S.slot_of[vm * st] = 0;
-        he = hmix(he, dbits(cur.t) ^ ((uint64_t)vm << 32));
+        he = hmix(he, dbits(ct) ^ ((uint64_t)vm << 32));
         if (DM == 1 && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
             if (P.dump.evict_model) P.dump.evict_model[dslot * P.dump.evict_cap + dn_ev] = vm;
-            if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = cur.t;
+            if (P.dump.evict_clock) P.dump.evict_clock[dslot * P.dump.evict_cap + dn_ev] = ct;
           }
           ++dn_ev;
         }
         ud = __ldg(&P.scen[sidx].unload_time_s);
       }
-      // start_load (engine.cpp:123-132), then blocked until LoadComplete
+      // start_load (engine.cpp:123-132), then blocked until its LoadComplete
       // (r, 0, .): completions strictly before r idle their slots.
       const double lt = K.lt[m];
-      const double r = (cur.t + ud) + lt;
-      lw = r - cur.t;
+      const double r = (ct + ud) + lt;
+      lw = r - ct;
       lo_sum += lt;
-      const int word = m | (K.lex[m] << 18);
-      S.word[v * st] = word;
+      S.slot[v * st].word = m | (K.lex[m] << 18);
       S.slot_of[m * st] = (uint8_t)(v + 1);
-      const double nr = -r;
-#pragma unroll
-      for (int s = 0; s < C; ++s)
-        if (stime[s] > nr) stime[s] = fabs(stime[s]);
-      cur = Cursor{r, 0, 0};
+      ct = r;
+      cw = 0u;
       hs = v;
     }
 
-    // start_service at now = cur.t (engine.cpp:134-153)
-    const double now = cur.t;
+    // start_service at now = ct (engine.cpp:134-153); its ServiceComplete is
+    // pushed with seq k (services start once per request, in order)
+    const double now = ct;
     const double qd = now - a;
     const double ttft = qd + pf;
     const double e2e = ttft + dc;
     const double done = (now + pf) + dc;
-#pragma unroll
-    for (int s = 0; s < C; ++s)
-      if (s == hs) stime[s] = -done;
-    S.done[hs * st] = done;
-    S.seq[hs * st] = k;  // push seq: services start once per request, in order
+    S.slot[hs * st].done = done;
+    S.slot[hs * st].seq = k;
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
       mttft = ttft > mttft ? ttft : mttft;
@@ -809,14 +757,16 @@ constexpr int LANE_BLOCK = 128;
 // [M or C][LANE_BLOCK], then per warp the record double buffer and the
 // window table.
 inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 * 8 + 2 * 4 + 4); }
+// 16-B aligned start of the per-lane columns
+inline __host__ __device__ size_t lane_smem_lane_off(int M) { return (lane_smem_cat(M) + 15) & ~(size_t)15; }
 inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
-  return (size_t)LANE_BLOCK * (M * 8 + C * 8 + M * 4 + 4 * 4 + C * 8 + M);
+  return (size_t)LANE_BLOCK * (M * 8 + C * sizeof(SlotEnt) + M * 4 + 4 * 4 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M, bool dump) {
   return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? (2 * kSampT * 32 + 32 + 2) * sizeof(double) : 0);  // 16-B multiple: keeps the next warp's records aligned
 }
 inline size_t lane_smem_bytes(int M, int C, bool dump) {
-  const size_t a = (((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
+  const size_t a = (lane_smem_lane_off(M) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
   return a + (LANE_BLOCK / 32) * lane_smem_warp(M, dump);
 }
 
@@ -840,17 +790,14 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   float* s_p2f = reinterpret_cast<float*>(s_tok + M);
   float* s_tokf = s_p2f + M;
   int* s_lex = reinterpret_cast<int*>(s_tokf + M);
-  // per-lane columns: 8-B ones first (M * 36 B of catalog keeps 4-B alignment only)
-  double* l_p4d = reinterpret_cast<double*>(smem + ((lane_smem_cat(M) + 7) & ~(size_t)7));  // [M][LB]
-  double* l_done = l_p4d + (size_t)M * LANE_BLOCK;                                          // [C][LB]
-  float* l_p4f = reinterpret_cast<float*>(l_done + (size_t)C * LANE_BLOCK);                // [M][LB]
-  float* l_prm = l_p4f + (size_t)M * LANE_BLOCK;                                  // [4][LANE_BLOCK]
-  uint32_t* l_seq = reinterpret_cast<uint32_t*>(l_prm + (size_t)4 * LANE_BLOCK);  // [C][LANE_BLOCK]
-  int* l_word = reinterpret_cast<int*>(l_seq + (size_t)C * LANE_BLOCK);          // [C][LANE_BLOCK]
-  uint8_t* l_slot = reinterpret_cast<uint8_t*>(l_word + (size_t)C * LANE_BLOCK);  // [M][LANE_BLOCK]
-  unsigned char* wbase =
-      smem + ((((lane_smem_cat(M) + 7) & ~(size_t)7) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
-      (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
+  // per-lane columns: 8- and 16-B ones first
+  double* l_p4d = reinterpret_cast<double*>(smem + lane_smem_lane_off(M));                  // [M][LB]
+  SlotEnt* l_slot = reinterpret_cast<SlotEnt*>(l_p4d + (size_t)M * LANE_BLOCK);             // [C][LB]
+  float* l_p4f = reinterpret_cast<float*>(l_slot + (size_t)C * LANE_BLOCK);                // [M][LB]
+  float* l_prm = l_p4f + (size_t)M * LANE_BLOCK;                                           // [4][LB]
+  uint8_t* l_sof = reinterpret_cast<uint8_t*>(l_prm + (size_t)4 * LANE_BLOCK);            // [M][LB]
+  unsigned char* wbase = smem + ((lane_smem_lane_off(M) + lane_smem_lane(M, C) + 15) & ~(size_t)15) +
+                         (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
   ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
   WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
   double* w_samp = reinterpret_cast<double*>(w_win + M);
@@ -874,11 +821,11 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   // happens, so the lookahead window is never read and is not maintained.
   const bool warp_win = __any_sync(kFull, need_win) && C < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
-  const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_done + threadIdx.x, l_prm + threadIdx.x,
-                   l_seq + threadIdx.x, l_word + threadIdx.x, l_slot + threadIdx.x, LANE_BLOCK,
-                   w_rec, w_win, w_samp};
+  const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_slot + threadIdx.x, l_prm + threadIdx.x,
+                   l_sof + threadIdx.x, LANE_BLOCK, w_rec, w_win, w_samp};
   replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
 }
 #endif  // CACE_HOST_EMULATION
 
 }  // namespace cace
+

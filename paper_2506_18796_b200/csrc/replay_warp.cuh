@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(WARP_BLOCK) replay_warp_kernel(ReplayParams P)
   const int64_t base = P.trace_off[sc.trace];
   const uint32_t n = (uint32_t)(P.trace_off[sc.trace + 1] - base);
   const ReqRec* tr = P.rec + base;
-  const int C = sc.num_accelerators * sc.models_per_accelerator;
+  const int C = (int)min((int64_t)sc.num_accelerators * sc.models_per_accelerator, (int64_t)M);  // effective_capacity
   const int variant = sc.variant;
   const bool is_lru = variant == CACE_LRU;
   const bool need_win = !is_lru && variant != CACE_MINUS_P3;

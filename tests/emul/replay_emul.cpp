@@ -49,11 +49,10 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
   std::vector<float> p4f(P.cat.M), prm(4);
-  std::vector<double> p4d(P.cat.M), done(C);
-  std::vector<uint32_t> seq(C);
-  std::vector<int> word(C);
+  std::vector<double> p4d(P.cat.M);
+  std::vector<SlotEnt> slot(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), p4d.data(), done.data(), prm.data(), seq.data(), word.data(), slot_of.data(), 1, nullptr, nullptr, nullptr};
+  const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), slot_of.data(), 1, nullptr, nullptr, nullptr};
   if (g_xr)
     replay_scenario<C, 2, D, true>(P, i, false, need_win, K, S);
   else
@@ -113,7 +112,7 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
         out[i].eviction_hash = out[i].outcome_hash = CACE_HASH_SEED;
         continue;
       }
-      const int Cap = sc[i].num_accelerators * sc[i].models_per_accelerator;
+      const int Cap = (int)effective_capacity(sc[i], cat.M);
       const bool D = dump_slot != nullptr;
       switch (Cap) {
 #define CASE(k) case k: D ? one<k, true>(P, i, K) : one<k, false>(P, i, K); break;

@@ -1,16 +1,19 @@
 #!/bin/bash
-# Bench alternative builds of the engine library: bash tools/gpu_variants.sh TAG exp/a.so exp/b.so ...
-# (each replaces lib/libcace_gpu.so for one config-4 bench + launch list; the original is restored)
+# A/B engine builds: config 4 at 1M and 131k scenarios (+ latency mode off), config 3.
+# Usage: bash tools/gpu_variants.sh TAG a.so b.so ...   (the in-tree library is "base")
 TAG=$1; shift
-OUT=gpurun_out
-mkdir -p $OUT
+OUT=gpurun_out; mkdir -p $OUT
 LIB=paper_2506_18796_b200/lib/libcace_gpu.so
-cp $LIB /tmp/orig.so
-for v in base "$@"; do
+cp $LIB /tmp/base.so
+for v in /tmp/base.so "$@"; do
   name=$(basename $v .so)
-  if [ "$v" != base ]; then cp $v $LIB; else cp /tmp/orig.so $LIB; fi
-  timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench_${TAG}_$name.log 2>&1
-  timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,sm__warps_active.avg.per_cycle_active,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $OUT/launches_${TAG}_$name.csv \
-    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+  cp $v $LIB
+  for args in "--seeds 32" "--seeds 4" "--config 3"; do
+    a=$(echo $args | tr -d ' -')
+    timeout 600 python bench.py $args --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | grep '^{' | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$a', 'lat=on', round(d['value']/1e9,2), round(d['ms_per_step'],1))" >> $OUT/variants_$TAG.txt
+    CACE_LATENCY_WAVES=0 timeout 600 python bench.py $args --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | grep '^{' | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$a', 'lat=off', round(d['value']/1e9,2), round(d['ms_per_step'],1))" >> $OUT/variants_$TAG.txt
+  done
 done
-cp /tmp/orig.so $LIB
+cp /tmp/base.so $LIB
