@@ -598,7 +598,7 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
     const char* v = std::getenv("CACE_LATENCY_WAVES");  // tuning override
     return v ? std::atoi(v) : 5;
   }();
-  const bool latency = lane_warps < (int64_t)waves * sms * (4 * LANE_BLOCK / 32);
+  const bool latency = lane_warps < (int64_t)waves * sms * (CACE_LANE_MIN_BLOCKS * LANE_BLOCK / 32);
   if (nseg > 0) {
     if (nseg > 1) fork_workers(e, s, nseg);
     for (size_t k = 0; k < nseg; ++k) {

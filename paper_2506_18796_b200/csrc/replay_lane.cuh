@@ -311,7 +311,7 @@ struct alignas(16) SlotEnt {
 // warp-shared tables.
 struct LaneSmem {
   float* p4f;        // [M] p2 + p4 = p2 + w1 * (tokens / normalizer), fp32 (screening)
-  double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67)
+  double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67); [M] unload_time_s
   SlotEnt* slot;     // [C] resident slots
   float* prm;        // [4] screen constants: 1/w, p1 scale, p1 offset, margin (+inf: no screen)
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
@@ -404,6 +404,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   // screen constants live in shared memory: read only by deciding lanes, so
   // they hold no registers across the replay loop
   // (fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0)
+  S.p4d[M * st] = sc.unload_time_s;  // read on evictions only
   S.prm[0] = 1.0f / (float)sc.window_length;
   S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
   S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
@@ -643,7 +644,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           }
           ++dn_ev;
         }
-        ud = __ldg(&P.scen[sidx].unload_time_s);
+        ud = S.p4d[M * st];  // unload_time_s
       }
       // start_load (engine.cpp:123-132), then blocked until its LoadComplete
       // (r, 0, .): completions strictly before r idle their slots.
@@ -750,7 +751,7 @@ constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 regi
 #ifndef CACE_HOST_EMULATION
 constexpr int LANE_BLOCK = 128;
 #ifndef CACE_LANE_MIN_BLOCKS
-#define CACE_LANE_MIN_BLOCKS 4  // <= 128 registers: 4 blocks (16 warps) per SM
+#define CACE_LANE_MIN_BLOCKS 5  // <= 96 registers: 5 blocks (20 warps) per SM
 #endif
 
 // Dynamic shared memory of one lane block: catalog columns, per-lane columns
@@ -760,7 +761,7 @@ inline __host__ __device__ size_t lane_smem_cat(int M) { return (size_t)M * (3 *
 // 16-B aligned start of the per-lane columns
 inline __host__ __device__ size_t lane_smem_lane_off(int M) { return (lane_smem_cat(M) + 15) & ~(size_t)15; }
 inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
-  return (size_t)LANE_BLOCK * (M * 8 + C * sizeof(SlotEnt) + M * 4 + 4 * 4 + M);
+  return (size_t)LANE_BLOCK * ((M + 1) * 8 + C * sizeof(SlotEnt) + M * 4 + 4 * 4 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M, bool dump) {
   return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? (2 * kSampT * 32 + 32 + 2) * sizeof(double) : 0);  // 16-B multiple: keeps the next warp's records aligned
@@ -771,7 +772,7 @@ inline size_t lane_smem_bytes(int M, int C, bool dump) {
 }
 
 // MINB = resident blocks per SM the register allocation targets:
-// CACE_LANE_MIN_BLOCKS (4: 16 warps/SM, 128 registers) for throughput on
+// CACE_LANE_MIN_BLOCKS (5: 20 warps/SM, 96 registers) for throughput on
 // large sweeps; 3 (12 warps/SM, up to 168 registers: a shorter per-request
 // dependency chain) when the sweep is only a few waves deep and every warp's
 // chain length bounds the step (capi.cu picks).
@@ -791,8 +792,8 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   float* s_tokf = s_p2f + M;
   int* s_lex = reinterpret_cast<int*>(s_tokf + M);
   // per-lane columns: 8- and 16-B ones first
-  double* l_p4d = reinterpret_cast<double*>(smem + lane_smem_lane_off(M));                  // [M][LB]
-  SlotEnt* l_slot = reinterpret_cast<SlotEnt*>(l_p4d + (size_t)M * LANE_BLOCK);             // [C][LB]
+  double* l_p4d = reinterpret_cast<double*>(smem + lane_smem_lane_off(M));                  // [M + 1][LB]
+  SlotEnt* l_slot = reinterpret_cast<SlotEnt*>(l_p4d + (size_t)(M + 1) * LANE_BLOCK);       // [C][LB]
   float* l_p4f = reinterpret_cast<float*>(l_slot + (size_t)C * LANE_BLOCK);                // [M][LB]
   float* l_prm = l_p4f + (size_t)M * LANE_BLOCK;                                           // [4][LB]
   uint8_t* l_sof = reinterpret_cast<uint8_t*>(l_prm + (size_t)4 * LANE_BLOCK);            // [M][LB]

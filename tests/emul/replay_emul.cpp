@@ -49,7 +49,7 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   const int v = P.scen[i].variant;
   const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
   std::vector<float> p4f(P.cat.M), prm(4);
-  std::vector<double> p4d(P.cat.M);
+  std::vector<double> p4d(P.cat.M + 1);
   std::vector<SlotEnt> slot(C);
   std::vector<uint8_t> slot_of(P.cat.M);
   const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), slot_of.data(), 1, nullptr, nullptr, nullptr};
