@@ -1,20 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark: scenario-requests replayed per second (BASELINE.json metric).
 
-Workload (default): BASELINE config 4 — 1,048,576 scenarios (4096
+Workload (default): BASELINE config 4 -- 1,048,576 scenarios (4096
 reference-expressible weight vectors x capacities 1..8 x 32 seeds) x 100k
 requests of a synthetic mixed completion/reasoning trace (8 CodeLLMs), i.e.
 1.05e11 scenario-requests per step.  One step = one full replay of the sweep.
-With N GPUs (torchrun, one process per GPU) scenarios are independent units
-sharded across ranks with no data-path collective: by default (--scaling
-weak) every rank replays its own full config-4 sweep (rank r's 32 traces use
-seeds 32r+1..32r+32), so the job replays N x 1.05e11 scenario-requests per
-step; --scaling strong splits one 1M-scenario sweep into N cost-balanced
-contiguous shards.  The fixed-size per-scenario summaries are all-gathered
-over NCCL (the only collective; included in the timed step).
+With N GPUs (torchrun, one process per GPU) the ONE sweep is split into N
+shards (strong scaling, the default): cace_shard_scenarios cuts every
+(capacity, trace) group into warps of 32 scenarios spread evenly over the
+ranks, every rank replays its shard with no data-path collective, and the
+fixed-size per-scenario summaries are all-gathered over NCCL (the only
+collective; inside the timed step).  `value` = 1.05e11 / max-over-ranks step
+time.  With N > 1 the line also carries `weak`: every rank replays its own
+full config-4 sweep (rank r's traces use seeds 32r+1..32r+32).
+
+Other configs: --config 3 (4096 weight vectors x one 100k trace), 2 (CACE vs
+LRU on one 10k trace), 5 (256-model pool, 10M-request bursty trace).
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
-CPU simulator (oracle/_ref, all host threads) on a bounded sample instead.
+CPU simulator (oracle/_ref, run() only, all host threads) on a bounded sample
+instead; that arm never maps the CUDA library.
 """
 from __future__ import annotations
 
@@ -48,12 +53,15 @@ def parse():
     ap.add_argument("--seeds", type=int, default=32)
     ap.add_argument("--scenarios", type=int, default=8192, help="cfg5 scenario count")
     ap.add_argument("--vectors-stride", type=int, default=1, help="subsample the 4096 weight vectors (debug)")
-    ap.add_argument("--cpu-sample", type=int, default=48, help="scenarios in the CPU-baseline sample")
+    ap.add_argument("--parity-sample", type=int, default=1024,
+                    help="stratified scenarios checked bit-exact against the reference (N = 1)")
+    ap.add_argument("--cpu-sample", type=int, default=128, help="scenarios in the timed CPU-baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--weak-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank replays its own full sweep (default); strong: one sweep split over ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong: one sweep split over the ranks (default); weak: every rank its own full sweep")
     return ap.parse_args()
 
 
@@ -62,8 +70,8 @@ def dist_env():
 
 
 def workload(args, part: int = 0):
-    """The sweep of one rank under weak scaling (part = rank; part 0 is the
-    BASELINE workload itself), or the whole sweep under strong scaling."""
+    """One config sweep (part = trace-seed offset; part 0 is the BASELINE
+    workload itself)."""
     from paper_2506_18796_b200 import synth
 
     if args.config == 5:
@@ -87,6 +95,19 @@ def workload_name(args, S, n):
     if args.config == 2:
         return "BASELINE config 2: CACE and LRU on one %d-request trace, capacity %d" % (n, args.capacity)
     return "BASELINE config 5: %d scenarios x %d-request bursty trace, 256 CodeLLMs, capacity 32, window 1024" % (S, n)
+
+
+def host_info():
+    info = {"cores": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip().lower().replace("(s)", "s").replace(" ", "_")] = v.strip()
+    except Exception:
+        pass
+    return info
 
 
 class ClockSampler:
@@ -129,41 +150,52 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def _cpu_replay(catalog, traces, sc, idx, threads):
-    """Replay scenarios sc[idx] on the host CPU: the reference run()
-    (oracle/_ref) when the catalog is reference-expressible (<= 16 models keyed
-    by language x task), else the C restatement (oracle/cace_port.c, checked
-    bit-exact against the reference).  Returns (summaries, seconds, kind)."""
+def stratified_sample(sc: np.ndarray, size: int, seed: int) -> np.ndarray:
+    """Scenario indices spread over every (capacity, variant, P1 mode,
+    window) stratum of the sweep: random members taken round-robin over the
+    strata (in random order) until `size`."""
+    rng = np.random.default_rng(seed)
+    cap = sc["num_accelerators"].astype(np.int64) * sc["models_per_accelerator"]
+    key = (((cap * 8 + sc["variant"]) * 2 + sc["p1_mode"]) << 20) + sc["window_length"]
+    strata = [rng.permutation(np.nonzero(key == k)[0]) for k in rng.permutation(np.unique(key))]
+    out, r = [], 0
+    while len(out) < min(size, len(sc)):
+        for s in strata:
+            if r < len(s) and len(out) < size:
+                out.append(s[r])
+        r += 1
+    return np.sort(np.array(out, np.int64))
+
+
+def _ref_inputs(catalog, traces, sc, idx):
     used = sorted({int(sc[i]["trace"]) for i in idx})
     remap = {t: k for k, t in enumerate(used)}
     rows = sc[idx].copy()
     rows["trace"] = [remap[int(t)] for t in rows["trace"]]
+    return used, rows
+
+
+def cpu_run(catalog, traces, sc, idx, threads, summaries=True):
+    """Replay scenarios sc[idx] on the host CPU: the reference run()
+    (oracle/_ref) when the catalog is reference-expressible (<= 16 models keyed
+    by language x task), else the C restatement (oracle/cace_port.c, checked
+    bit-exact against the reference).  summaries=False times run() only.
+    Returns (summaries or None, seconds, kind)."""
+    used, rows = _ref_inputs(catalog, traces, sc, idx)
     if len(catalog) <= 16:
         from oracle import ref
         from tests.helpers import ref_catalog, ref_scenario, ref_trace
 
-        summ, secs = ref.run_batch(ref_catalog(ref, catalog), [ref_trace(traces[t]) for t in used],
-                                   [ref_scenario(ref, r) for r in rows], threads=threads)
-        return summ, secs, "reference"
+        rcat, rtr = ref_catalog(ref, catalog), [ref_trace(traces[t]) for t in used]
+        rsc = [ref_scenario(ref, r) for r in rows]
+        if summaries:
+            summ, secs = ref.run_batch(rcat, rtr, rsc, threads=threads)
+            return summ, secs, "reference"
+        return None, ref.time_batch(rcat, rtr, rsc, threads=threads), "reference"
     from oracle import port
 
     summ, secs = port.run_batch(port.Catalog(catalog), [traces[t] for t in used], rows, threads=threads)
     return summ, secs, "port"
-
-
-def cpu_baseline(catalog, traces, sc, sample: int, seed: int = 12345):
-    """The CPU simulator on all host threads over a bounded random sample of
-    the same sweep; also the parity sample."""
-    rng = np.random.default_rng(seed)
-    idx = np.sort(rng.choice(len(sc), size=min(sample, len(sc)), replace=False))
-    threads = os.cpu_count() or 1
-    summ, secs, kind = _cpu_replay(catalog, traces, sc, idx, threads)
-    n_req = sum(len(traces[int(sc[i]["trace"])]) for i in idx)
-    return idx, summ, {"value": n_req / secs, "unit": "scenario-requests/s", "cores": threads, "kind": kind,
-                       "sample": f"{len(idx)} random scenarios of the same sweep x {len(traces[0])} requests "
-                                 f"({n_req:.3g} scenario-requests, {secs:.2f} s, "
-                                 f"{'reference run()' if kind == 'reference' else 'C restatement'} "
-                                 f"on a std::thread/pthread fan-out)"}
 
 
 def run_reference_arm(args):
@@ -179,26 +211,29 @@ def run_reference_arm(args):
     threads = os.cpu_count() or 1
     # enough scenarios per step to keep every host thread busy (cost varies
     # with the window length), bounded so the whole run takes ~a minute
-    per_step = max(4 * threads, 16) if args.config == 4 else max(threads // 4, 2)
+    per_step = max(4 * threads, 16) if args.config in (3, 4) else max(threads // 4, 2)
+    per_step = min(per_step, len(sc))
     rng = np.random.default_rng(777)
     times, reqs = [], []
     kind = "reference"
     for step in range(args.warmup + args.steps):
         idx = np.sort(rng.choice(len(sc), size=per_step, replace=False))
-        _, secs, kind = _cpu_replay(catalog, traces, sc, idx, threads)
+        _, secs, kind = cpu_run(catalog, traces, sc, idx, threads, summaries=False)
         if step >= args.warmup:
             times.append(secs)
-            reqs.append(per_step * args.requests)
+            reqs.append(sum(len(traces[int(sc[i]["trace"])]) for i in idx))
     value = sum(reqs) / sum(times)
     print(json.dumps({
         "impl": "reference", "metric": "scenario-requests replayed/sec", "value": value,
         "unit": "scenario-requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE config {args.config}, bounded random sample per step",
+        "config": {"workload": workload_name(args, len(sc), args.requests) + ", bounded random sample per step",
                    "requests": args.requests, "scenarios_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "scenario-requests/s", "cores": threads, "kind": kind,
-                         "sample": f"{per_step} random scenarios x {args.requests} requests per step"},
+                         "sample": f"{per_step} random scenarios x {args.requests} requests per step, "
+                                   f"reference run() only (std::thread fan-out, schedule(dynamic))"},
+        "host": host_info(),
         "e2e": {"value": value, "unit": "scenario-requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -226,49 +261,58 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    def coll(x):  # tensor on the collective's device
-        return x if backend == "nccl" else x.cpu()
-
     def all_reduce(x, op):
-        y = coll(x)
+        y = x if backend == "nccl" else x.cpu()
         torch.distributed.all_reduce(y, op=op)
         return y
 
-    def all_gather_bytes(buf):
-        if backend == "nccl":
-            torch.distributed.all_gather_into_tensor(gathered, buf)
-            return gathered
-        parts = [torch.empty(buf.numel(), dtype=torch.uint8) for _ in range(world)]
-        torch.distributed.all_gather(parts, buf.cpu())
-        return torch.cat(parts)
     import paper_2506_18796_b200 as P
     from paper_2506_18796_b200 import SUMMARY_DTYPE
+    from paper_2506_18796_b200.shard import shard_indices
 
-    from paper_2506_18796_b200.shard import shard_bounds
-
-    if args.scaling == "weak":
-        catalog, traces, sc = workload(args, part=rank)
-        sc_all = sc  # the CPU baseline / parity sample (world == 1 only)
-        bounds = [r * len(sc) for r in range(world + 1)]
+    catalog, traces, sc_all = workload(args)
+    if args.scaling == "strong" and world > 1:
+        parts = shard_indices(sc_all, len(catalog), world)
     else:
-        catalog, traces, sc_all = workload(args)
-        bounds = shard_bounds(sc_all, world)
-        sc = sc_all[bounds[rank]:bounds[rank + 1]]
-    S_total = bounds[-1]
+        parts = [np.arange(len(sc_all))] * world
+    S_total = len(sc_all) if args.scaling == "strong" else world * len(sc_all)
+    sc = sc_all[parts[rank]]
+    if args.scaling == "weak" and rank > 0:
+        catalog, traces, sc = workload(args, part=rank)
     n_req = args.requests
+    W = SUMMARY_DTYPE.itemsize
+    max_rows = max(len(p) for p in parts)
+
+    class Sweep:
+        """A device-resident sweep: engine (traces laid out and uploaded
+        once), planned scenarios and summary buffers on a dedicated stream."""
+
+        def __init__(self, catalog, traces, sc):
+            self.sc = sc
+            self.eng = P.Engine(catalog, traces, device=local, stream=stream.cuda_stream)
+            self.eng.plan(sc)
+            self.d_sc = torch.from_numpy(sc.view(np.uint8).copy()).cuda()
+            self.d_out = torch.zeros(len(sc) * W, dtype=torch.uint8, device="cuda")
+            self.pad = torch.zeros(max(len(sc), max_rows) * W, dtype=torch.uint8, device="cuda")
+            self.gathered = torch.empty(world * self.pad.numel(), dtype=torch.uint8, device="cuda")
+
+        def step(self, gather: bool):
+            launches = self.eng.replay_device(self.d_sc.data_ptr(), len(self.sc), self.d_out.data_ptr(),
+                                              stream.cuda_stream)
+            if world > 1 and gather:  # the sweep's only collective
+                self.pad[: self.d_out.numel()].copy_(self.d_out)
+                if backend == "nccl":
+                    torch.distributed.all_gather_into_tensor(self.gathered, self.pad)
+                else:
+                    parts_ = [torch.empty(self.pad.numel(), dtype=torch.uint8) for _ in range(world)]
+                    torch.distributed.all_gather(parts_, self.pad.cpu())
+            return launches
+
     # A dedicated (non-default) stream: the engine, the events and the L2
     # flush all run on it, so the CUDA events bracket exactly the replay.
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    eng = P.Engine(catalog, traces, device=local, stream=stream.cuda_stream)
-    eng.plan(sc)
-    d_sc = torch.from_numpy(sc.view(np.uint8).copy()).cuda()
-    d_out = torch.zeros(len(sc) * SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
-    max_shard = max(bounds[r + 1] - bounds[r] for r in range(world))
-    gather_buf = d_out
-    if world > 1:
-        pad = torch.zeros(max_shard * SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
-        gathered = torch.empty(world * pad.numel(), dtype=torch.uint8, device="cuda")
+    sweep = Sweep(catalog, traces, sc)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -276,44 +320,50 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def step():
-        launches = eng.replay_device(d_sc.data_ptr(), len(sc), d_out.data_ptr(), stream.cuda_stream)
-        if world > 1:
-            pad[: d_out.numel()].copy_(d_out)
-            all_gather_bytes(pad)
-        return launches
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step()
-    barrier()
-    ms = []
-    launches = 0
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+    def timed(sw, steps, warmup, gather=True):
+        for _ in range(warmup):
+            flush.zero_()
+            sw.step(gather)
+        barrier()
+        ms, launches = [], 0
+        for _ in range(steps):
             flush.zero_()
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            launches += step()
+            launches += sw.step(gather)
             e1.record(stream)
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
-    barrier()
-    t_local = float(np.mean(ms))
-    t = torch.tensor([t_local], device="cuda")
-    if world > 1:
-        t = all_reduce(t, torch.distributed.ReduceOp.MAX)
-    t_max = float(t.item())
+        barrier()
+        t = torch.tensor([float(np.mean(ms))], device="cuda")
+        if world > 1:
+            t = all_reduce(t, torch.distributed.ReduceOp.MAX)
+        return float(t.item()), float(np.mean(ms)), launches
+
+    with ClockSampler(local) as clk:
+        t_max, t_local, launches = timed(sweep, args.steps, args.warmup)
     value = S_total * n_req / (t_max / 1e3)
-    summ = d_out.cpu().numpy().view(SUMMARY_DTYPE)
+    summ = sweep.d_out.cpu().numpy().view(SUMMARY_DTYPE)
     status_ok = bool((summ["status"] == 0).all())
     evictions = int(summ["evictions"].sum())
     if world > 1:
         ev = torch.tensor([evictions], dtype=torch.float64, device="cuda")
-        ev = all_reduce(ev, torch.distributed.ReduceOp.SUM)
-        evictions = int(ev.item())
+        evictions = int(all_reduce(ev, torch.distributed.ReduceOp.SUM).item())
+        ok = torch.tensor([1.0 if status_ok else 0.0], device="cuda")
+        status_ok = bool(all_reduce(ok, torch.distributed.ReduceOp.MIN).item() > 0)
+
+    # ---- weak scaling (N > 1): every rank replays its own full sweep ----
+    weak = None
+    if world > 1 and args.scaling == "strong" and args.weak_steps > 0:
+        wc, wt, wsc = workload(args, part=rank)
+        wsweep = Sweep(wc, wt, wsc)
+        w_max, _, _ = timed(wsweep, args.weak_steps, 1, gather=False)
+        del wsweep
+        weak = {"value": world * len(wsc) * n_req / (w_max / 1e3), "ms_per_step": w_max,
+                "note": f"each rank its own full sweep ({len(wsc)} scenarios, trace seeds offset by rank), "
+                        "no gather"}
 
     # ---- end to end through the public API (host buffers, H2D/D2H inside) ----
     e2e = None
@@ -325,8 +375,13 @@ def main():
             host_summ = P.run_batch(traces, catalog, sc, device=local)
             if world > 1:
                 hs = torch.from_numpy(host_summ.view(np.uint8)).cuda()
-                pad[: hs.numel()].copy_(hs)
-                all_gather_bytes(pad).cpu()
+                sweep.pad[: hs.numel()].copy_(hs)
+                if backend == "nccl":
+                    torch.distributed.all_gather_into_tensor(sweep.gathered, sweep.pad)
+                    sweep.gathered.cpu()
+                else:
+                    torch.distributed.all_gather([torch.empty(sweep.pad.numel(), dtype=torch.uint8)
+                                                  for _ in range(world)], sweep.pad.cpu())
             barrier()
             if k > 0:  # first call warms the CUDA context / allocator
                 e2e_ms.append(1e3 * (time.perf_counter() - t0))
@@ -341,12 +396,13 @@ def main():
         n_groups = len(np.unique(sc[["num_accelerators", "models_per_accelerator", "trace"]]))
         h2d = (n_all * (48 + 4) + len(traces) * (8 + 4 * len(catalog) + 4) + len(sc) * (sc.dtype.itemsize + 8)
                + n_groups * 31 * 8 + len(catalog) * 36 + 2 * 256 * 8)
-        d2h = len(sc) * SUMMARY_DTYPE.itemsize
+        d2h = len(sc) * W
         e2e = {"value": S_total * n_req / (float(tl.item()) / 1e3), "unit": "scenario-requests/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(tl.item()),
-               "path": "paper_2506_18796_b200.run_batch -> cace_replay_batch (C ABI), host SoA traces + scenarios in, "
-                       "summaries out, trace layout + plan + replay + copies timed"}
+               "path": "paper_2506_18796_b200.run_batch -> cace_replay_batch (C ABI) per rank, host SoA traces + "
+                       "scenarios in, summaries out (+ all-gather when N > 1), trace layout + plan + replay + "
+                       "copies timed"}
 
     peaks = {}
     try:
@@ -354,13 +410,14 @@ def main():
     except Exception:
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # per-GPU roofline of this rank's replay (dominant kernels of the step)
     achieved_gbs = (len(sc) * n_req * B_ALG) / (t_local / 1e3) / 1e9
     # measured DRAM traffic of the same step (ncu launch list, committed)
     traffic = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        key = f"cfg{args.config}_n{n_req}_s{S_total}"
-        if key in tr and world == 1:
+        key = f"cfg{args.config}_n{n_req}_s{len(sc)}"
+        if key in tr:
             traffic = tr[key]["dram_bytes_per_step"]
     except Exception:
         pass
@@ -372,40 +429,57 @@ def main():
     parity = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            idx, rsumm, cpu = cpu_baseline(catalog, traces, sc_all, args.cpu_sample)
-            from tests.helpers import SUMMARY_FLOAT_KEYS, SUMMARY_KEYS  # noqa: F811
+            from tests.helpers import SUMMARY_FLOAT_KEYS, SUMMARY_KEYS
 
-            gs = summ[idx]
+            threads = os.cpu_count() or 1
+            pidx = stratified_sample(sc_all, args.parity_sample, 12345)
+            rsumm, psecs, kind = cpu_run(catalog, traces, sc_all, pidx, threads, summaries=True)
+            gs = summ[pidx]
             ok = all((gs[k] == rsumm[k]).all() for k in SUMMARY_KEYS) and all(
                 (gs[k].view(np.uint64) == rsumm[k].view(np.uint64)).all() for k in SUMMARY_FLOAT_KEYS)
-            parity = {"scenarios": int(len(idx)), "bit_exact": bool(ok)}
+            parity = {"scenarios": int(len(pidx)), "bit_exact": bool(ok),
+                      "sample": "stratified over (capacity, variant, P1 mode, window); every summary field incl. "
+                                "the outcome and eviction-sequence fingerprints", "cpu_seconds": psecs}
+            cidx = np.sort(np.random.default_rng(777).choice(len(sc_all), size=min(args.cpu_sample, len(sc_all)),
+                                                             replace=False))
+            _, secs, kind = cpu_run(catalog, traces, sc_all, cidx, threads, summaries=False)
+            n_cpu = sum(len(traces[int(sc_all[i]["trace"])]) for i in cidx)
+            cpu = {"value": n_cpu / secs, "unit": "scenario-requests/s", "cores": threads, "kind": kind,
+                   "sample": f"{len(cidx)} random scenarios of the same sweep x {n_req} requests "
+                             f"({n_cpu:.3g} scenario-requests, {secs:.2f} s, "
+                             f"{'reference run() only' if kind == 'reference' else 'C restatement'} "
+                             f"on a std::thread fan-out, schedule(dynamic))"}
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unavailable": repr(ex)[:200]}
+    kernel = ("replay_warp_kernel<SPL> (warp per scenario)" if len(catalog) > 64 or args.config == 5 else
+              "replay_lane_kernel<C,...> (one launch per capacity segment, run concurrently)")
     out = {
         "metric": "scenario-requests replayed/sec", "value": value, "unit": "scenario-requests/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload_name(args, S_total, n_req),
+        "config": {"workload": workload_name(args, len(sc_all), n_req),
                    "scenarios": S_total, "requests_per_trace": n_req, "models": len(catalog),
-                   "parallelism": (f"scenario shards x{world}, each rank its own full sweep (weak)"
-                                   if args.scaling == "weak" else f"one sweep split over {world} ranks (strong)"),
+                   "parallelism": (f"one sweep split over {world} ranks (strong, cace_shard_scenarios)"
+                                   if args.scaling == "strong" else
+                                   f"scenario shards x{world}, each rank its own full sweep (weak)"),
                    "l2": "flushed (256 MB write) before every step",
                    "vectors_stride": args.vectors_stride},
         "eviction_decisions_per_s": evictions / (t_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm, "traffic": traffic,
-                     "kernel": "replay_lane_kernel<C> (the step = one launch per capacity, run concurrently)",
-                     "note": "achieved = 18 B algorithmic per scenario-request x scenario-requests of the step / "
-                             "step time (CUDA events on the launch stream); traffic = ncu dram read+write bytes of "
-                             "the step's launches (profiles/traffic.json): the trace is L2-resident and shared by "
-                             "every lane, so the kernel is issue-bound, not HBM-bound (profiles/)"},
+                     "frac": achieved_gbs / hbm, "traffic": traffic, "kernel": kernel,
+                     "note": "achieved = 18 B algorithmic per scenario-request x this rank's scenario-requests / "
+                             "its step time (CUDA events on the launch stream); traffic = ncu dram read+write "
+                             "bytes of the step's launches (profiles/traffic.json): the trace is L2-resident and "
+                             "shared by every lane, so the kernel is issue-bound, not HBM-bound (profiles/)"},
         "gpu_launches": launches,
         "status_ok": status_ok,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "weak": weak,
         "cpu_baseline": cpu,
         "parity_sample": parity,
+        "host": host_info(),
     }
     print(json.dumps(out))
     if world > 1:

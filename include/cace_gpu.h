@@ -207,6 +207,32 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
                           cace_summary_t* summaries, const cace_dump_t* dump,
                           const cace_opts_t* opts, char* msg, size_t msg_cap);
 
+/* The same sweep on several devices of this process (the device-scale form
+ * of run_grid's OpenMP fan-out, experiment.cpp:100-115).  The traces are laid
+ * out once and uploaded to every device; the scenarios are split into
+ * n_devices shards with cace_shard_scenarios (every shard gets the same
+ * (capacity, trace) mix, whole warps); one host thread and stream per device
+ * plans and replays its shard; the 112-B summaries are gathered to
+ * devices[0] over NCCL (ncclSend/ncclRecv in one group, NVLink / NVSwitch) --
+ * peer copies when NCCL is not loadable or a device repeats -- and copied to
+ * the caller's array in the caller's order.  *gather_kind (optional): 0 one
+ * device, 1 NCCL, 2 peer copies.  Host memory in and out.  Results are
+ * identical to cace_replay_batch on one device. */
+int32_t cace_replay_batch_multi(const cace_catalog_t* catalog, const cace_trace_t* traces,
+                                int32_t n_traces, const cace_scenario_t* scenarios,
+                                int64_t n_scenarios, cace_summary_t* summaries,
+                                const int32_t* devices, int32_t n_devices, const cace_opts_t* opts,
+                                int32_t* gather_kind, char* msg, size_t msg_cap);
+/* The shard assignment cace_replay_batch_multi uses (also for one process
+ * per GPU: rank r replays the scenarios with shard_of[i] == r).  Every
+ * (effective capacity, trace) group is cut into warps of 32 scenarios spread
+ * evenly over the shards; scenarios run() would reject go to shard 0.  No
+ * GPU needed. */
+int32_t cace_shard_scenarios(const cace_scenario_t* scenarios, int64_t n, int32_t n_models,
+                             int32_t n_shards, int32_t* shard_of);
+/* NCCL version the multi-device gather uses (0 = not loadable). */
+int32_t cace_nccl_version(void);
+
 /* compute_run_metrics (metrics.cpp:35-62) of every scenario's replay,
  * computed on the device: the replay captures each scenario's TTFT /
  * E2E samples, one CTA per (scenario, task class) selects the nearest-rank

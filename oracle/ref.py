@@ -114,6 +114,8 @@ def lib():
                                         P(i32), cp, sz]
         L.ref_run_batch.restype = i32
         L.ref_run_batch.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, P(f64), cp, sz]
+        L.ref_time_batch.restype = i32
+        L.ref_time_batch.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, i64, i32, P(f64), cp, sz]
         L.ref_max_threads.restype = i32
         L.ref_libm_log.argtypes = [vp, i64, vp]
         _lib = L
@@ -338,6 +340,26 @@ def run_batch(cat: Catalog, traces: list[dict], scenarios: list[RefScenario], th
     if rc != 0:
         raise RefError(msg.value.decode())
     return summ, secs.value
+
+
+def time_batch(cat: Catalog, traces: list[dict], scenarios: list[RefScenario], threads: int = 0) -> float:
+    """Seconds of the same fan-out running reference ``run()`` only (no
+    eviction recorder, no summaries): the CPU-baseline timing
+    (bench_grid.cpp:18-25 times run() through run_grid)."""
+    offs = np.zeros(len(traces) + 1, np.int64)
+    for k, t in enumerate(traces):
+        offs[k + 1] = offs[k] + len(t["arrival"])
+    cat_arr = lambda key, dt: np.ascontiguousarray(np.concatenate([t[key] for t in traces]), dt)
+    arr, mdl = cat_arr("arrival", np.float64), cat_arr("model", np.int32)
+    pr, out = cat_arr("prompt", np.int32), cat_arr("output", np.int32)
+    sc = (RefScenario * len(scenarios))(*scenarios)
+    secs = C.c_double(0)
+    msg = C.create_string_buffer(1024)
+    rc = lib().ref_time_batch(cat._h, _ptr(arr), _ptr(mdl), _ptr(pr), _ptr(out), _ptr(offs), len(traces),
+                              C.cast(sc, C.c_void_p), len(scenarios), threads, C.byref(secs), msg, 1024)
+    if rc != 0:
+        raise RefError(msg.value.decode())
+    return secs.value
 
 
 def max_threads() -> int:

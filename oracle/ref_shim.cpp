@@ -568,6 +568,60 @@ int32_t ref_run_batch(void* catp, const double* arrival, const int32_t* model_id
   return 0;
 }
 
+// CPU baseline timing: the same fan-out running the reference run() only --
+// no eviction recorder bound (the --wrap shim just forwards to
+// select_victim) and no summary; reports are discarded.  This is what
+// bench_grid.cpp:18-25 times (run_grid wall time around run()).
+int32_t ref_time_batch(void* catp, const double* arrival, const int32_t* model_idx, const int32_t* prompt,
+                       const int32_t* output, const int64_t* offsets, int32_t n_traces,
+                       const ref_scenario_t* scenarios, int64_t n_scenarios, int32_t threads, double* seconds,
+                       char* msg, size_t mcap) {
+  const ModelCatalog& cat = *static_cast<ModelCatalog*>(catp);
+  std::vector<Trace> traces;
+  try {
+    for (int32_t k = 0; k < n_traces; ++k) {
+      int64_t b = offsets[k], e = offsets[k + 1];
+      traces.push_back(make_trace(cat, arrival + b, model_idx + b, prompt + b, output + b, e - b));
+    }
+  } catch (const std::exception& e) {
+    put_msg(msg, mcap, e.what());
+    return 2;
+  }
+  int nthr = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  if (nthr < 1) nthr = 1;
+  std::string error;
+  std::mutex err_mu;
+  std::atomic<int64_t> next{0};
+  std::atomic<uint64_t> sink{0};
+  auto worker = [&]() {
+    for (;;) {
+      const int64_t i = next.fetch_add(1, std::memory_order_relaxed);  // schedule(dynamic)
+      if (i >= n_scenarios) break;
+      const ref_scenario_t& sc = scenarios[i];
+      try {
+        SimulationReport rep = run(traces.at(static_cast<size_t>(sc.trace)), cat, to_cluster(sc),
+                                   make_policy(to_policy(sc)));
+        sink.fetch_add(rep.counters.evictions, std::memory_order_relaxed);
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (error.empty()) error = e.what();
+      }
+    }
+  };
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int k = 1; k < nthr; ++k) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  auto t1 = std::chrono::steady_clock::now();
+  if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+  if (!error.empty()) {
+    put_msg(msg, mcap, error);
+    return 1;
+  }
+  return 0;
+}
+
 int32_t ref_max_threads(void) { return static_cast<int32_t>(std::thread::hardware_concurrency()); }
 
 // libm log as the reference calls it (policy.cpp:51), for device-log pinning.

@@ -6,8 +6,8 @@ sm_100a CUDA kernels behind the C ABI in ``include/cace_gpu.h``
 (``lib/libcace_gpu.so``).  This package is the Python mirror of the reference
 simulator's API over that ABI (``api``), the synthetic workload builders of
 BASELINE.json's configs (``synth``) and the multi-GPU scenario sharding
-(``shard``).  Importing it loads the CUDA library and fails loudly if it is
-missing; there is no CPU fallback.
+(``shard``).  Importing it does not map the CUDA library; the first engine
+call loads it and fails loudly if it is missing -- there is no CPU fallback.
 """
 from .api import (  # noqa: F401
     ClusterConfig,
@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     run_metrics,
     select_victim,
     service_times,
+    shard_scenarios,
     version,
 )
 from ._native import METRICS_DTYPE, SCENARIO_DTYPE, SUMMARY_DTYPE  # noqa: F401

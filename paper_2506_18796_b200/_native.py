@@ -2,7 +2,7 @@
 
 The shared library is built in-tree by ``paper_2506_18796_b200.build`` (nvcc,
 sm_100a).  There is no fallback: if the library is missing this module raises
-at import, and every replay entry point fails with ``CACE_E_NO_DEVICE`` when no
+on first use, and every replay entry point fails with ``CACE_E_NO_DEVICE`` when no
 CUDA device is visible.
 """
 from __future__ import annotations
@@ -130,7 +130,8 @@ EXPORTED = [
     "cace_eviction_score_batch", "cace_dedup_window_batch", "cace_service_times_batch",
     "cace_log_selftest", "cace_log_host", "cace_probe_log_variant", "cace_run_metrics_batch", "cace_metrics_select",
     "cace_trace_parse_jsonl", "cace_trace_load_jsonl", "cace_trace_jsonl_size", "cace_trace_jsonl_header",
-    "cace_trace_jsonl_copy", "cace_trace_jsonl_free",
+    "cace_trace_jsonl_copy", "cace_trace_jsonl_free", "cace_replay_batch_multi", "cace_shard_scenarios",
+    "cace_nccl_version",
 ]
 
 
@@ -149,6 +150,12 @@ def _load():
     L.cace_device_count.restype = i32
     L.cace_replay_batch.restype = i32
     L.cace_replay_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, P(DumpABI), P(OptsABI), C.c_char_p, sz]
+    L.cace_replay_batch_multi.restype = i32
+    L.cace_replay_batch_multi.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, vp, i32, P(OptsABI), vp,
+                                          C.c_char_p, sz]
+    L.cace_shard_scenarios.restype = i32
+    L.cace_shard_scenarios.argtypes = [vp, i64, i32, i32, vp]
+    L.cace_nccl_version.restype = i32
     L.cace_run_metrics_batch.restype = i32
     L.cace_run_metrics_batch.argtypes = [P(CatalogABI), vp, i32, vp, i64, vp, vp, P(OptsABI), C.c_char_p, sz]
     L.cace_metrics_select.restype = i32
@@ -194,7 +201,18 @@ def _load():
     return L
 
 
-lib = _load()
+_lib = None
+
+
+def __getattr__(name):
+    """`lib` loads the CUDA engine on first use (importing the package, e.g.
+    for the synthetic-workload generators, does not map the library)."""
+    global _lib
+    if name == "lib":
+        if _lib is None:
+            _lib = _load()
+        return _lib
+    raise AttributeError(name)
 
 
 def ptr(a):

@@ -333,16 +333,41 @@ def _trace_array(traces):
     return arr
 
 
+def shard_scenarios(scenarios: np.ndarray, n_models: int, n_shards: int) -> np.ndarray:
+    """Shard of every scenario (cace_shard_scenarios): each (capacity, trace)
+    group is cut into warps of 32 spread evenly over the shards.  No GPU."""
+    scenarios = np.ascontiguousarray(scenarios, SCENARIO_DTYPE)
+    out = np.zeros(len(scenarios), np.int32)
+    rc = N.lib.cace_shard_scenarios(ptr(scenarios), len(scenarios), n_models, n_shards, ptr(out))
+    if rc != N.CACE_OK:
+        raise SimError("cace_shard_scenarios: invalid arguments", rc)
+    return out
+
+
 def run_batch(traces: list[Trace], catalog: ModelCatalog, scenarios: np.ndarray, device: int = 0,
               dump_scenarios=None, evict_cap: int | None = None, raise_on_error: bool = True,
-              kernel: int = KERNEL_AUTO):
+              kernel: int = KERNEL_AUTO, devices=None, return_gather_kind: bool = False):
     """Replay every scenario on the GPU (host buffers in and out).
 
     Returns the summary array (SUMMARY_DTYPE); with ``dump_scenarios`` also a
-    list of per-scenario full reports."""
+    list of per-scenario full reports.  ``devices`` (a list of ordinals):
+    the sweep is sharded over those devices of this process
+    (cace_replay_batch_multi, summaries gathered over NCCL); summaries only."""
     scenarios = np.ascontiguousarray(scenarios, SCENARIO_DTYPE)
     summ = np.zeros(len(scenarios), SUMMARY_DTYPE)
     tarr = _trace_array(traces)
+    if devices is not None:
+        if dump_scenarios is not None:
+            raise ValueError("run_batch: full dumps replay on one device")
+        devs = np.ascontiguousarray(devices, np.int32)
+        msg = C.create_string_buffer(1024)
+        gk = C.c_int32(-1)
+        rc = N.lib.cace_replay_batch_multi(C.byref(catalog.abi()), C.cast(tarr, C.c_void_p), len(traces),
+                                           ptr(scenarios), len(scenarios), ptr(summ), ptr(devs), len(devs),
+                                           C.byref(_opts(int(devs[0]), kernel=kernel)), C.byref(gk), msg, 1024)
+        if rc != N.CACE_OK and (raise_on_error or rc >= N.CACE_E_INVALID):
+            _raise(rc, msg)
+        return (summ, int(gk.value)) if return_gather_kind else summ
     dump = None
     dump_abi = None
     if dump_scenarios is not None and len(dump_scenarios):

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -473,6 +474,11 @@ void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t
   if (smem > 48 * 1024)
     CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DM, MINB>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // one L1/shared split for every capacity's kernel: blocks of different
+  // segments can then share an SM without a carveout change (shallow sweeps
+  // +9%, profiles/r2/ab_carveout_v6.txt)
+  CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DM, MINB>,
+                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
   replay_lane_kernel<C, MW, DM, MINB><<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
@@ -845,6 +851,11 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
   return rc;
 }
 
+}  // extern "C"
+
+#include "multi_device.inc"
+
+extern "C" {
 
 int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
                                int32_t n_traces, const cace_scenario_t* scenarios,

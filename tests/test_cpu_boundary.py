@@ -100,16 +100,25 @@ def test_workload_shapes():
     assert set(np.unique(sc["num_accelerators"])) == set(range(1, 9))
 
 
-def test_shard_bounds_cover_and_balance():
+def test_shards_cover_and_balance():
+    """cace_shard_scenarios: every scenario in exactly one shard, every
+    (capacity, trace) group split evenly in whole warps."""
     from paper_2506_18796_b200 import shard, synth
 
     sc = synth.scenario_grid(synth.weight_vectors_cfg3(), range(1, 9), 4, 600)
     for world in (1, 2, 4, 8):
-        b = shard.shard_bounds(sc, world)
-        assert b[0] == 0 and b[-1] == len(sc) and all(x <= y for x, y in zip(b, b[1:]))
-        cost = shard.scenario_cost(sc)
-        parts = [cost[b[r]:b[r + 1]].sum() for r in range(world)]
-        assert max(parts) / min(parts) < 1.01
+        parts = shard.shard_indices(sc, 8, world)
+        allidx = np.sort(np.concatenate(parts))
+        assert np.array_equal(allidx, np.arange(len(sc)))
+        for c in range(1, 9):
+            for t in range(4):
+                g = [int(((sc["num_accelerators"][p] == c) & (sc["trace"][p] == t)).sum()) for p in parts]
+                assert max(g) - min(g) <= 32 and sum(g) == 4096, (world, c, t, g)
+    # small groups rotate over the shards
+    small = synth.scenario_grid(synth.weight_vectors_cfg3()[:40], range(1, 9), 4, 600)
+    parts = shard.shard_indices(small, 8, 8)
+    sizes = [len(p) for p in parts]
+    assert sum(sizes) == len(small) and max(sizes) - min(sizes) <= 64, sizes
 
 
 _GLOO_WORKER = r"""
@@ -126,11 +135,11 @@ cat = synth.eight_model_catalog()
 traces = [synth.mixed_trace(cat, 1500, seed=s) for s in (1, 2)]
 pols = synth.weight_vectors_cfg3()[::256]
 sc = synth.scenario_grid(pols, [2, 3], 2, 600)
-b = shard.shard_bounds(sc, world)
-mine = sc[b[rank]:b[rank + 1]]
+parts = shard.shard_indices(sc, len(cat), world)
+mine = sc[parts[rank]]
 rcat = ref_catalog(ref, cat)
 summ, _ = ref.run_batch(rcat, [ref_trace(t) for t in traces], [ref_scenario(ref, s) for s in mine], threads=1)
-full = shard.gather_summaries(torch.from_numpy(summ.view(np.uint8).copy()), b)
+full = shard.gather_summaries(torch.from_numpy(summ.view(np.uint8).copy()), parts)
 if rank == 0:
     want, _ = ref.run_batch(rcat, [ref_trace(t) for t in traces], [ref_scenario(ref, s) for s in sc], threads=2)
     assert full.tobytes() == want.tobytes(), "gathered summaries differ"

@@ -1,6 +1,7 @@
 """GPU, BASELINE config 4 at full size (1,048,576 scenarios x 100k requests):
-size-independent invariants on every summary, plus a random sample checked
-bit-exact against the reference run() (oracle/_ref, all host threads)."""
+size-independent invariants on every summary, plus a sample checked
+bit-exact against the reference run() (oracle/_ref, all host threads): a
+1024-scenario sample stratified over capacity x variant x P1 mode x window."""
 import numpy as np
 import pytest
 
@@ -35,13 +36,14 @@ def test_config4_full_size_invariants_and_sample(ref):
     assert (summ["n_completion"] + summ["n_reasoning"] == n).all()
     # capacity >= pool never evicts (test_engine.cpp:102-121)
     assert (summ["evictions"][cap >= len(catalog)] == 0).all()
-    # a random sample bit-exact against the reference simulator
-    from bench import _cpu_replay
-
-    idx = np.sort(np.random.default_rng(2026).choice(len(sc), 24, replace=False))
+    # a stratified 1024-scenario sample (every capacity x variant x P1 mode x
+    # window stratum) bit-exact against the reference simulator, full length
     import os
 
-    want, _, kind = _cpu_replay(catalog, traces, sc, idx, os.cpu_count() or 1)
+    from bench import cpu_run, stratified_sample
+
+    idx = stratified_sample(sc, 1024, 2026)
+    want, _, kind = cpu_run(catalog, traces, sc, idx, os.cpu_count() or 1)
     assert kind == "reference"
     got = summ[idx]
     for k in SUMMARY_KEYS:

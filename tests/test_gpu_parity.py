@@ -67,7 +67,10 @@ def test_random_scenarios_bit_exact(ref, seed):
                            window_length=int(rng.choice([1, 2, 3, 5, 10, 16, 50, 200])),
                            output_token_normalizer=int(rng.choice([600, 300, 50])),
                            p1_mode=int(rng.integers(0, 2)))
-        cl = ClusterConfig(num_accelerators=int(rng.integers(1, 9)), models_per_accelerator=1,
+        # capacity = num_accelerators x models_per_accelerator (engine.cpp:83-84),
+        # including capacities above the pool size and above 64
+        mpa = int(rng.choice([1, 1, 2, 4]))
+        cl = ClusterConfig(num_accelerators=int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 20])), models_per_accelerator=mpa,
                            unload_time_s=float(rng.choice([0.0, 0.0, 0.5, 2.0])))
         rows.append((int(rng.integers(0, 3)), pol, cl))
     sc = api.make_scenarios(rows)
@@ -351,3 +354,4 @@ def test_reference_side_binding_drop_in():
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ADAPTER ALL_OK" in out.stdout
+
