@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--weak-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "lane", "warp"],
+                    help="engine kernel mapping (auto = the planner's choice)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong: one sweep split over the ranks (default); weak: every rank its own full sweep")
     return ap.parse_args()
@@ -270,6 +272,7 @@ def main():
     from paper_2506_18796_b200 import SUMMARY_DTYPE
     from paper_2506_18796_b200.shard import shard_indices
 
+    kernel_opt = {"auto": P.api.KERNEL_AUTO, "lane": P.api.KERNEL_LANE, "warp": P.api.KERNEL_WARP}[args.kernel]
     catalog, traces, sc_all = workload(args)
     if args.scaling == "strong" and world > 1:
         parts = shard_indices(sc_all, len(catalog), world)
@@ -289,7 +292,7 @@ def main():
 
         def __init__(self, catalog, traces, sc):
             self.sc = sc
-            self.eng = P.Engine(catalog, traces, device=local, stream=stream.cuda_stream)
+            self.eng = P.Engine(catalog, traces, device=local, stream=stream.cuda_stream, kernel=kernel_opt)
             self.eng.plan(sc)
             self.d_sc = torch.from_numpy(sc.view(np.uint8).copy()).cuda()
             self.d_out = torch.zeros(len(sc) * W, dtype=torch.uint8, device="cuda")
@@ -372,7 +375,7 @@ def main():
         for k in range(args.e2e_steps + 1):
             barrier()
             t0 = time.perf_counter()
-            host_summ = P.run_batch(traces, catalog, sc, device=local)
+            host_summ = P.run_batch(traces, catalog, sc, device=local, kernel=kernel_opt)
             if world > 1:
                 hs = torch.from_numpy(host_summ.view(np.uint8)).cuda()
                 sweep.pad[: hs.numel()].copy_(hs)
@@ -451,8 +454,12 @@ def main():
                              f"on a std::thread fan-out, schedule(dynamic))"}
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unavailable": repr(ex)[:200]}
-    kernel = ("replay_warp_kernel<SPL> (warp per scenario)" if len(catalog) > 64 or args.config == 5 else
-              "replay_lane_kernel<C,...> (one launch per capacity segment, run concurrently)")
+    if args.kernel == "warp" or len(catalog) > 256:
+        kernel = "replay_warp_kernel<SPL> (warp per scenario)"
+    elif len(catalog) > 64:
+        kernel = "replay_lane_wide_kernel<MW,DM> (lane per scenario, wide pools, one warp per block)"
+    else:
+        kernel = "replay_lane_kernel<C,...> (one launch per capacity segment, run concurrently)"
     out = {
         "metric": "scenario-requests replayed/sec", "value": value, "unit": "scenario-requests/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
@@ -464,7 +471,7 @@ def main():
                                    if args.scaling == "strong" else
                                    f"scenario shards x{world}, each rank its own full sweep (weak)"),
                    "l2": "flushed (256 MB write) before every step",
-                   "vectors_stride": args.vectors_stride},
+                   "vectors_stride": args.vectors_stride, "kernel": args.kernel},
         "eviction_decisions_per_s": evictions / (t_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": achieved_gbs / hbm, "traffic": traffic, "kernel": kernel,

@@ -256,9 +256,10 @@ struct cace_engine {
   // plan
   int64_t plan_n = -1;
   struct Seg {
-    int C;      // lane kernel: capacity template; warp kernel: slots per lane (1 or 2)
+    int C;      // lane kernel: capacity; warp kernel: slots per lane (1 or 2)
     int64_t b, e;
     bool warp;  // warp-per-scenario kernel
+    bool wide;  // lane kernel, wide-pool mode (pools > 64 models or capacities > 16)
   };
   std::vector<Seg> segs;
   std::vector<int64_t> h_order;  // plan entries (scenario index | kShadowBit)
@@ -340,23 +341,23 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->bad_code.clear();
   auto capof = [&](int64_t i) { return (int)effective_capacity(sc[i], e->cat.M); };
   // Kernel choice: lane-per-scenario for capacities <= 16 and pools <= 64
-  // models (register-resident slots and window); warp-per-scenario otherwise
-  // (BASELINE config 5 regime) or when forced with CACE_KERNEL_WARP.
+  // models (register-resident slots and window, capacity a template
+  // parameter); the same lane kernel in wide-pool mode for capacities <= 32
+  // and pools <= 256 (BASELINE config 5); warp-per-scenario beyond that or
+  // when forced with CACE_KERNEL_WARP.
   const bool force_warp = e->kernel_pref == CACE_KERNEL_WARP;
-  const bool force_lane = e->kernel_pref == CACE_KERNEL_LANE;
-  auto use_warp = [&](int64_t i) {
-    const bool lane_ok = capof(i) <= kMaxLaneC && e->cat.M <= kLaneMaxModels;
-    if (force_warp || !lane_ok) return true;
-    if (force_lane) return false;
-    return false;
-  };
-  auto key = [&](int64_t i) {  // segment key: (kernel, template parameter)
+  const int M0 = e->cat.M;
+  // dense segment key: 1..16 lane capacity, 17..48 wide-lane capacity + 16,
+  // 49..50 warp kernel (slots per lane)
+  auto key = [&](int64_t i) {
     const int C = capof(i);
-    return use_warp(i) ? 1000 + (C <= 32 ? 1 : 2) : C;
+    if (!force_warp && C <= kMaxLaneC && M0 <= kLaneMaxModels) return C;
+    if (!force_warp && C <= kWideC && M0 <= kWideMaxModels) return 16 + C;
+    return 48 + (C <= 32 ? 1 : 2);
   };
   // Per scenario, on all host threads: the run() preconditions, the dense
-  // segment key (1..16 lane capacities, 17..18 warp kernel; -1 = invalid) and
-  // a compact coherence key (trace, variant, p1_mode, window).
+  // segment key (-1 = invalid) and a compact coherence key (trace, variant,
+  // p1_mode, window).
   std::vector<int32_t> status(n);
   std::vector<int8_t> kv(n);
   std::vector<uint64_t> ck(n);
@@ -373,8 +374,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
           kv[i] = -1;
           continue;
         }
-        const int K = key(i);
-        kv[i] = (int8_t)(K >= 1000 ? kMaxLaneC + (K - 1000) : K);
+        kv[i] = (int8_t)key(i);
         const uint32_t win = (uint32_t)std::min(sc[i].window_length, (1 << 27) - 1);
         ck[i] = ((uint64_t)(uint32_t)sc[i].trace << 32) | ((uint64_t)(sc[i].variant & 7) << 29) |
                 ((uint64_t)(sc[i].p1_mode & 1) << 28) | win;
@@ -395,7 +395,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   // common case for generated sweeps).
   std::vector<int64_t> ok;
   {
-    const int kmax = kMaxLaneC + 2;
+    const int kmax = 50;
     std::vector<int64_t> cnt(kmax + 2, 0);
     for (int64_t i = 0; i < n; ++i) {
       if (kv[i] < 0) {
@@ -422,10 +422,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   // write nothing) so each warp is trace-uniform and walks its trace in
   // lockstep.  Warp segments need no padding (one warp = one scenario).
   // (segment key and trace read from the compact per-scenario arrays)
-  auto seg_of = [&](int64_t i) {
-    const int d = kv[i];
-    return d > kMaxLaneC ? 1000 + (d - kMaxLaneC) : d;
-  };
+  auto seg_of = [&](int64_t i) { return (int)kv[i]; };
   auto trace_of = [&](int64_t i) { return (int32_t)(ck[i] >> 32); };
   std::vector<int64_t> order;
   order.reserve(ok.size() + ok.size() / 8 + 32 * 64);
@@ -433,9 +430,9 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
     const int K = seg_of(ok[k]);
     const int64_t seg_b = (int64_t)order.size();
     size_t j = k;
-    if (K >= 1000) {
+    if (K > 48) {
       while (j < ok.size() && seg_of(ok[j]) == K) order.push_back(ok[j++]);
-      e->segs.push_back({K - 1000, seg_b, (int64_t)order.size(), true});
+      e->segs.push_back({K - 48, seg_b, (int64_t)order.size(), true, false});
     } else {
       while (j < ok.size() && seg_of(ok[j]) == K) {
         const int32_t t = trace_of(ok[j]);
@@ -445,7 +442,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
         for (int64_t q = 0; q < pad; ++q) order.push_back(ok[j] | (int64_t)kShadowBit);
         j = g;
       }
-      e->segs.push_back({K, seg_b, (int64_t)order.size(), false});
+      e->segs.push_back({K > 16 ? K - 16 : K, seg_b, (int64_t)order.size(), false, K > 16});
     }
     k = j;
   }
@@ -529,6 +526,44 @@ void dispatch_lane(int dm, int C, const ReplayParams& P, int64_t count, size_t s
   }
 }
 
+constexpr int kWideG = 8;  // lanes per scenario of the wide-pool lane kernel (C / G = 4 slots per lane)
+
+template <int MW, int DM>
+void launch_lane_wide(const ReplayParams& P, int64_t count, cudaStream_t s) {
+  constexpr int G = kWideG;
+  const size_t smem = lane_wide_smem_bytes(P.cat.M, DM != 0, G);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(replay_lane_wide_kernel<MW, DM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  CK(cudaFuncSetAttribute(replay_lane_wide_kernel<MW, DM, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  constexpr int SB = LANE_BLOCK_WIDE / G;  // scenarios (plan entries) per block
+  const unsigned grid = (unsigned)((count + SB - 1) / SB);
+  replay_lane_wide_kernel<MW, DM, G><<<grid, LANE_BLOCK_WIDE, smem, s>>>(P);
+  CK(cudaGetLastError());
+}
+
+template <int DM>
+void dispatch_lane_wide_dm(const ReplayParams& P, int64_t count, cudaStream_t s) {
+  const int M = P.cat.M;
+  if (M <= 32)
+    launch_lane_wide<1, DM>(P, count, s);
+  else if (M <= 64)
+    launch_lane_wide<2, DM>(P, count, s);
+  else if (M <= 128)
+    launch_lane_wide<4, DM>(P, count, s);
+  else
+    launch_lane_wide<8, DM>(P, count, s);
+}
+
+void dispatch_lane_wide(int dm, const ReplayParams& P, int64_t count, cudaStream_t s) {
+  if (dm == 0)
+    dispatch_lane_wide_dm<0>(P, count, s);
+  else if (dm == 1)
+    dispatch_lane_wide_dm<1>(P, count, s);
+  else
+    dispatch_lane_wide_dm<2>(P, count, s);
+}
+
 ReplayParams replay_params(const cace_engine* e, const cace_scenario_t* d_sc, cace_summary_t* d_out,
                            const DumpDev& dump) {
   ReplayParams P{};
@@ -558,6 +593,8 @@ void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams 
   const int dm = !dump_on ? 0 : (P.dump.samples ? 2 : 1);
   if (g.warp)
     dispatch_warp(dump_on, g.C, P, end - b, ws);
+  else if (g.wide)
+    dispatch_lane_wide(dm, P, end - b, ws);
   else
     dispatch_lane(dm, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, latency);
 }

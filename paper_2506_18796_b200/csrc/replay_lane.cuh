@@ -311,9 +311,11 @@ struct alignas(16) SlotEnt {
 // warp-shared tables.
 struct LaneSmem {
   float* p4f;        // [M] p2 + p4 = p2 + w1 * (tokens / normalizer), fp32 (screening)
-  double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67); [M] unload_time_s
+  double* p4d;       // [M] p4 = w1 * (tokens / normalizer), exact fp64 (policy.cpp:66-67) (NULL: wide)
   SlotEnt* slot;     // [C] resident slots
   float* prm;        // [4] screen constants: 1/w, p1 scale, p1 offset, margin (+inf: no screen)
+  double* ud;        // [1] unload_time_s (read on evictions)
+  float* wprm;       // [2] wide pools: p2 scale (0 / 1), w1 / normalizer (fp32; 0 when p4 is ablated)
   uint8_t* slot_of;  // [M] slot + 1 holding model m, 0 = not resident
   int stride;
   ReqRec* rec;       // warp: record double buffer [64]
@@ -366,9 +368,22 @@ __device__ __forceinline__ void flush_samples(const double* tile, double* const*
 // XR: the exact fallback as rolled loops over the idle slots re-reading the
 // shared slot table (compact code, few live registers) or unrolled over the
 // slot entries already in registers.
-template <int C, int MW, int DM, bool XR = true>
+// WIDE (pools > 64 models or capacities > 16): C is the unroll bound and the
+// capacity is cap_rt (<= C); no per-lane p2 + p4 tables -- the fp32 screen
+// forms p2 + p4 from the block's catalog columns and two per-lane scalars,
+// the exact path recomputes p4 = w1 * (tokens / normalizer).
+template <int C, int MW, int DM, bool XR = true, bool WIDE = false, int G = 1>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
-                                const CatShared& K, const LaneSmem& S) {
+                                const CatShared& K, const LaneSmem& S, int cap_rt = C) {
+  static_assert(G == 1 || WIDE, "lane groups are a wide-pool mode");
+  const int cap = WIDE ? cap_rt : C;
+#ifdef CACE_HOST_EMULATION
+  const int lig = 0;
+  const unsigned gmask = 1u;
+#else
+  const int lig = (int)(threadIdx.x & (G - 1));  // lane within the scenario's group
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+#endif
   const cace_scenario_t sc = P.scen[sidx];
   const int M = P.cat.M;
   const int64_t base = P.trace_off[sc.trace];
@@ -395,27 +410,37 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     if (!is_lru) {
       const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[mm];
       const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[mm] / norm);
-      S.p4d[mm * st] = p4;
-      S.p4f[mm * st] = (float)(p2 + p4);
-      screen_ok = screen_ok && fabs(p2 + p4) <= 1e5;  // false for NaN / inf
-      if (screen_ok) tbound = fmaxf(tbound, 2.0f + fabsf((float)(p2 + p4)));
+      if (!WIDE) {
+        S.p4d[mm * st] = p4;
+        S.p4f[mm * st] = (float)(p2 + p4);
+      }
+      const double b = WIDE ? fabs(p2) + fabs(p4) : fabs(p2 + p4);
+      screen_ok = screen_ok && b <= 1e5;  // false for NaN / inf
+      if (screen_ok) tbound = fmaxf(tbound, 2.0f + (float)b);
     }
+  }
+  if (WIDE) {
+    // fp32 p2 + p4 = fma(p4s, tokens, p2s * p2): the roundings of p2, w1 /
+    // normalizer and the fma add <= 2^-22 (|p2| + |p4|) to the screen's
+    // error, covered by the doubled coefficient of the margin below
+    S.wprm[0] = variant == CACE_MINUS_P2 ? 0.0f : 1.0f;
+    S.wprm[st] = variant == CACE_MINUS_P4 ? 0.0f : (float)(sc.w1 / norm);
   }
   // screen constants live in shared memory: read only by deciding lanes, so
   // they hold no registers across the replay loop
   // (fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0)
-  S.p4d[M * st] = sc.unload_time_s;  // read on evictions only
+  S.ud[0] = sc.unload_time_s;  // read on evictions only
   S.prm[0] = 1.0f / (float)sc.window_length;
   S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
   S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
-  S.prm[3 * st] = screen_ok ? 6e-5f + 1e-6f * (tbound + 4.0f) : INFINITY;
+  S.prm[3 * st] = screen_ok ? 6e-5f + (WIDE ? 2e-6f : 1e-6f) * (tbound + 4.0f) : INFINITY;
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
   bool dump_outcomes = false;
   double* samples = nullptr;  // this scenario's metrics samples
   uint32_t ncomp_t = 0;
-  if (DM != 0 && !shadow) {
+  if (DM != 0 && !shadow && lig == 0) {  // one lane of a group writes
     dslot = P.dump.slot[sidx];
     if (dslot >= 0) doff = P.dump.dump_off[dslot];
     if (DM == 1)
@@ -486,9 +511,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     } else {
       int v;
       double ud = 0.0;
-      if (occ < C) {  // free slot, no unload delay (engine.cpp:184-187)
+      if (occ < cap) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
       } else {
+        if constexpr (!WIDE) {
         // Full: the Idle residents are the eviction candidates
         // (engine.cpp:189-208, policy.cpp:85-89).
         double sd[C];
@@ -497,6 +523,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         unsigned idm = 0;
 #pragma unroll
         for (int s = 0; s < C; ++s) {
+          if (WIDE && s >= cap) break;
           const SlotEnt e = S.slot[s * st];
           sd[s] = e.done;
           sq[s] = e.seq;
@@ -511,12 +538,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           double t1 = sd[0];
           uint32_t q1 = sq[0];
 #pragma unroll
-          for (int s = 1; s < C; ++s)
+          for (int s = 1; s < C; ++s) {
+            if (WIDE && s >= cap) break;
             if (sd[s] < t1 || (sd[s] == t1 && sq[s] < q1)) {
               s1 = s;
               t1 = sd[s];
               q1 = sq[s];
             }
+          }
           ct = t1;
           cw = kKindSC | q1;
           v = s1;
@@ -532,6 +561,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             int flex = 0;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
+              if (WIDE && s >= cap) break;
               const int lx = slot_lex(sw[s]);
               if ((idm >> s) & 1u)
                 if (f < 0 || sd[s] < flu || (sd[s] == flu && lx < flex)) {
@@ -553,11 +583,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             // term conversions and three fp32 sums add <= 2^-21 (|T| + 4).
             // The margin is twice the worst case.
             const float rcpw = S.prm[0], p1s = S.prm[st], p1o = S.prm[2 * st];
+            const float p2s = WIDE ? S.wprm[0] : 0.0f, p4s = WIDE ? S.wprm[st] : 0.0f;
             float best = -INFINITY, second = -INFINITY;
             int bs = 0;
             const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
+              if (WIDE && s >= cap) break;
               const int ms = slot_model(sw[s]);
               const float t = fmaxf((float)(now - sd[s]), 1.0f);  // max(d, 1) in fp32
               const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
@@ -567,7 +599,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 const WinEnt e = win.gather(ms);
                 p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
               }
-              float T = (p1 + p3) + S.p4f[ms * st];  // p2 + p4 pre-summed
+              float T = (p1 + p3) + (WIDE ? fmaf(p4s, K.tokf[ms], p2s * K.p2f[ms])
+                                          : S.p4f[ms * st]);  // p2 + p4 pre-summed
               T = ((idm >> s) & 1u) ? T : -INFINITY;
               bs = T > best ? s : bs;
               second = fmaxf(second, fminf(best, T));
@@ -605,7 +638,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                   const WinEnt e = win.gather(ms);
                   p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
                 }
-                const double p4 = S.p4d[ms * st];
+                const double p4 = !WIDE ? S.p4d[ms * st]
+                                        : (variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm));
                 const double T = ((p1 + p2) + p3) + p4;
                 if (T == T && (bv < 0 || T > bt || (T == bt && (lu < blu || (lu == blu && lx < blex))))) {
                   bt = T;
@@ -633,6 +667,170 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             }
           }
         }
+        } else {
+          // ---- wide pools: the scenario's G lanes split its slots (lane
+          // lig owns slots lig + G j) and combine partial results with
+          // shuffles inside the group ----
+          constexpr int J = C / G;
+          double ld[J];
+          uint32_t lq[J];
+          int lwd[J];
+          unsigned idm = 0;
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const int s = lig + G * j;
+            ld[j] = INFINITY;
+            lq[j] = 0xffffffffu;
+            lwd[j] = 0;
+            if (s < cap) {
+              const SlotEnt e = S.slot[s * st];
+              ld[j] = e.done;
+              lq[j] = e.seq;
+              lwd[j] = e.word;
+              idm |= sc_popped(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
+            }
+          }
+#pragma unroll
+          for (int o = 1; o < G; o <<= 1) idm |= __shfl_xor_sync(gmask, idm, o);
+          if (idm == 0) {
+            // every resident busy: the min-key ServiceComplete's slot
+            double t1 = INFINITY;
+            uint32_t q1 = 0xffffffffu;
+            int s1 = 0;
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+              if (ld[j] < t1 || (ld[j] == t1 && lq[j] < q1)) {
+                t1 = ld[j];
+                q1 = lq[j];
+                s1 = lig + G * j;
+              }
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+              const double ot = __shfl_xor_sync(gmask, t1, o);
+              const uint32_t oq = __shfl_xor_sync(gmask, q1, o);
+              const int os = __shfl_xor_sync(gmask, s1, o);
+              if (ot < t1 || (ot == t1 && oq < q1)) {
+                t1 = ot;
+                q1 = oq;
+                s1 = os;
+              }
+            }
+            ct = t1;
+            cw = kKindSC | q1;
+            v = s1;
+          } else if ((idm & (idm - 1u)) == 0) {
+            v = __ffs(idm) - 1;  // exactly one candidate
+          } else {
+            const double now = ct;
+            if (is_lru) {
+              // sorted-first = min (last_used, lex) over idle (policy.cpp:92-100)
+              double flu = INFINITY;
+              int flex = 0x7fffffff, f = 0;
+#pragma unroll
+              for (int j = 0; j < J; ++j) {
+                const int s = lig + G * j;
+                const int lx = slot_lex(lwd[j]);
+                if ((idm >> s) & 1u)
+                  if (ld[j] < flu || (ld[j] == flu && lx < flex)) {
+                    flu = ld[j];
+                    flex = lx;
+                    f = s;
+                  }
+              }
+#pragma unroll
+              for (int o = 1; o < G; o <<= 1) {
+                const double ou = __shfl_xor_sync(gmask, flu, o);
+                const int ox = __shfl_xor_sync(gmask, flex, o);
+                const int of = __shfl_xor_sync(gmask, f, o);
+                if (ou < flu || (ou == flu && ox < flex)) {
+                  flu = ou;
+                  flex = ox;
+                  f = of;
+                }
+              }
+              v = f;
+            } else {
+              // fp32 screen over the lane's own idle slots, then the group's
+              // (best, second, arg-best); the margin test is as in the
+              // one-lane path (an fp32 tie leaves best - second = 0)
+              const float rcpw = S.prm[0], p1s = S.prm[st], p1o = S.prm[2 * st];
+              const float p2s = S.wprm[0], p4s = S.wprm[st];
+              float best = -INFINITY, second = -INFINITY;
+              int bs = 0x7fffffff;
+              const uint32_t wend = k + w;
+#pragma unroll
+              for (int j = 0; j < J; ++j) {
+                const int s = lig + G * j;
+                if (!((idm >> s) & 1u)) continue;
+                const int ms = slot_model(lwd[j]);
+                const float t = fmaxf((float)(now - ld[j]), 1.0f);  // max(d, 1) in fp32
+                const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
+                const float p1 = fmaf(p1s, p1v, p1o);
+                float p3 = 0.0f;
+                if (need_win) {
+                  const WinEnt e = win.gather(ms);
+                  p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
+                }
+                const float T = (p1 + p3) + fmaf(p4s, K.tokf[ms], p2s * K.p2f[ms]);
+                bs = T > best ? s : bs;
+                second = fmaxf(second, fminf(best, T));
+                best = fmaxf(best, T);
+              }
+#pragma unroll
+              for (int o = 1; o < G; o <<= 1) {
+                const float ob = __shfl_xor_sync(gmask, best, o);
+                const float os2 = __shfl_xor_sync(gmask, second, o);
+                const int obs = __shfl_xor_sync(gmask, bs, o);
+                second = fmaxf(fmaxf(second, os2), fminf(best, ob));
+                bs = best > ob ? bs : (ob > best ? obs : (obs < bs ? obs : bs));
+                best = fmaxf(best, ob);
+              }
+              v = bs;
+              if (!(best - second > S.prm[3 * st])) {
+                // exact fp64 path (policy.cpp:39-78, 92-113): every lane of
+                // the group walks all idle slots (identical result, no reduction)
+                int f = -1;
+                double flu = 0.0;
+                int flex = 0;
+                double bt = 0.0, blu = 0.0;
+                int blex = 0, bv = -1;
+                bool f_nan = false;
+#pragma unroll 1
+                for (unsigned q = idm; q; q &= q - 1u) {
+                  const int s = __ffs(q) - 1;
+                  const double lu = S.slot[s * st].done;
+                  const int wd = S.slot[s * st].word;
+                  const int ms = slot_model(wd);
+                  const int lx = slot_lex(wd);
+                  const double p1 = variant == CACE_MINUS_P1
+                                        ? 0.0
+                                        : exact_p1(now, lu, verbatim, P.log_variant, P.log_tab, P.log_tab2);
+                  const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
+                  double p3 = 0.0;
+                  if (variant != CACE_MINUS_P3) {
+                    const WinEnt e = win.gather(ms);
+                    p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
+                  }
+                  const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm);
+                  const double T = ((p1 + p2) + p3) + p4;
+                  if (f < 0 || lu < flu || (lu == flu && lx < flex)) {  // sorted-first so far
+                    f = s;
+                    flu = lu;
+                    flex = lx;
+                    f_nan = T != T;
+                  }
+                  if (T == T && (bv < 0 || T > bt || (T == bt && (lu < blu || (lu == blu && lx < blex))))) {
+                    bt = T;
+                    blu = lu;
+                    blex = lx;
+                    bv = s;
+                  }
+                }
+                v = f_nan ? f : bv;
+              }
+            }
+          }
+        }
         // residents.erase(victim); evictions++ (engine.cpp:205-206)
         const int vm = slot_model(S.slot[v * st].word);
         S.slot_of[vm * st] = 0;
@@ -644,7 +842,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           }
           ++dn_ev;
         }
-        ud = S.p4d[M * st];  // unload_time_s
+        ud = S.ud[0];  // unload_time_s
       }
       // start_load (engine.cpp:123-132), then blocked until its LoadComplete
       // (r, 0, .): completions strictly before r idle their slots.
@@ -724,7 +922,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       flush_samples(S.samp + kSampT * 32, samp_ptrs(S.samp), (int64_t)nco + nre - nre % kSampT, nre % kSampT);
   }
 #endif
-  if (shadow) return;
+  if (shadow || lig != 0) return;
   cace_summary_t o;
   o.hits = hits;
   o.misses = n - hits;
@@ -823,8 +1021,79 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const bool warp_win = __any_sync(kFull, need_win) && C < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_slot + threadIdx.x, l_prm + threadIdx.x,
-                   l_sof + threadIdx.x, LANE_BLOCK, w_rec, w_win, w_samp};
+                   l_p4d + (size_t)M * LANE_BLOCK + threadIdx.x, nullptr, l_sof + threadIdx.x, LANE_BLOCK,
+                   w_rec, w_win, w_samp};
   replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
+}
+
+// ---- wide pools / capacities ----------------------------------------------
+// Pools of up to 256 models (window in MW <= 8 registers per lane) and
+// capacities up to kWideC: the lane-per-scenario replay with the capacity a
+// runtime value under an unroll bound of kWideC, no per-lane p2 + p4 tables
+// (replay_scenario<..., WIDE>), and a GROUP of G lanes per scenario: lane lig
+// of a group owns slots lig + G j, so an eviction decision scans C / G slots
+// per lane and combines the group's partial results with log2(G) shuffle
+// rounds (BASELINE config 5: capacity 32, 8 lanes x 4 slots).  A warp holds
+// 32 / G scenarios of one trace; the lookahead window stays warp-wide.
+constexpr int LANE_BLOCK_WIDE = 128;
+constexpr int kWideC = 32;
+constexpr int kWideMaxModels = 256;
+inline __host__ __device__ size_t lane_wide_lane(int M, int G) {
+  return (size_t)(LANE_BLOCK_WIDE / G) * (kWideC * sizeof(SlotEnt) + 8 + 4 * 4 + 2 * 4 + M);
+}
+inline size_t lane_wide_smem_bytes(int M, bool dump, int G) {
+  const size_t a = (lane_smem_lane_off(M) + lane_wide_lane(M, G) + 15) & ~(size_t)15;
+  return a + (LANE_BLOCK_WIDE / 32) * lane_smem_warp(M, dump);
+}
+
+template <int MW, int DM, int G>
+__global__ void __launch_bounds__(LANE_BLOCK_WIDE, 4) replay_lane_wide_kernel(ReplayParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int C = kWideC, SB = LANE_BLOCK_WIDE / G;  // scenarios per block
+  const int M = P.cat.M;
+  double* s_lt = reinterpret_cast<double*>(smem);
+  double* s_p2 = s_lt + M;
+  double* s_tok = s_p2 + M;
+  float* s_p2f = reinterpret_cast<float*>(s_tok + M);
+  float* s_tokf = s_p2f + M;
+  int* s_lex = reinterpret_cast<int*>(s_tokf + M);
+  // per-scenario columns (SB wide), shared by the scenario's G lanes
+  SlotEnt* l_slot = reinterpret_cast<SlotEnt*>(smem + lane_smem_lane_off(M));  // [C][SB]
+  double* l_ud = reinterpret_cast<double*>(l_slot + (size_t)C * SB);          // [1][SB]
+  float* l_prm = reinterpret_cast<float*>(l_ud + SB);                         // [4][SB]
+  float* l_wprm = l_prm + 4 * SB;                                             // [2][SB]
+  uint8_t* l_sof = reinterpret_cast<uint8_t*>(l_wprm + 2 * SB);               // [M][SB]
+  unsigned char* wbase = smem + ((lane_smem_lane_off(M) + lane_wide_lane(M, G) + 15) & ~(size_t)15) +
+                         (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
+  ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
+  WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
+  double* w_samp = reinterpret_cast<double*>(w_win + M);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    s_lt[m] = P.cat.load_time[m];
+    s_p2[m] = P.cat.p2[m];
+    s_tok[m] = P.cat.tokens[m];
+    s_p2f[m] = (float)P.cat.p2[m];
+    s_tokf[m] = (float)P.cat.tokens[m];
+    s_lex[m] = P.cat.lex[m];
+  }
+  __syncthreads();
+  const int col = threadIdx.x / G;  // the scenario's column in the block
+  const int64_t gi = P.seg_begin + (int64_t)blockIdx.x * SB + col;
+  const int64_t wfirst = P.seg_begin + (int64_t)blockIdx.x * SB + (threadIdx.x & ~31) / G;
+  if (wfirst >= P.seg_end) return;  // whole warps (the plan pads groups to 32 scenarios)
+  const uint64_t e = (uint64_t)P.order[gi];
+  const bool shadow = (e & kShadowBit) != 0;
+  const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
+  const cace_scenario_t& sc = P.scen[sidx];
+  const int variant = sc.variant;
+  // the warp's scenarios share the effective capacity (planner groups by it)
+  const int cap = (int)min((int64_t)sc.num_accelerators * sc.models_per_accelerator, (int64_t)M);
+  const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
+  const bool warp_win = __any_sync(kFull, need_win) && cap < M;
+  const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
+  const LaneSmem S{nullptr, nullptr, l_slot + col, l_prm + col, l_ud + col, l_wprm + col, l_sof + col, SB,
+                   w_rec, w_win, w_samp};
+  replay_scenario<C, MW, DM, true, true, G>(P, sidx, shadow, warp_win, K, S, cap);
 }
 #endif  // CACE_HOST_EMULATION
 

@@ -33,6 +33,7 @@ static inline unsigned __float_as_uint(float f) { unsigned u; std::memcpy(&u, &f
 #define __logf(x) logf(x)
 static inline float __fdividef(float a, float b) { return a / b; }
 static inline int __ffs(unsigned x) { return __builtin_ffs((int)x); }
+template <typename T> static inline T __shfl_xor_sync(unsigned, T x, int) { return x; }  // groups of one lane
 
 #include "../../paper_2506_18796_b200/csrc/replay_lane.cuh"
 #include "../../paper_2506_18796_b200/csrc/layout.hpp"
@@ -52,11 +53,29 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   std::vector<double> p4d(P.cat.M + 1);
   std::vector<SlotEnt> slot(C);
   std::vector<uint8_t> slot_of(P.cat.M);
-  const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), slot_of.data(), 1, nullptr, nullptr, nullptr};
+  const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), p4d.data() + P.cat.M, nullptr, slot_of.data(),
+                   1, nullptr, nullptr, nullptr};
   if (g_xr)
     replay_scenario<C, 2, D, true>(P, i, false, need_win, K, S);
   else
     replay_scenario<C, 2, D, false>(P, i, false, need_win, K, S);
+}
+
+// The wide-pool mode (pools up to 256 models, capacity <= 32 at run time).
+template <bool D>
+static void one_wide(const ReplayParams& P, int64_t i, const CatShared& K, int cap) {
+  const int v = P.scen[i].variant;
+  const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
+  std::vector<float> prm(4), wprm(2);
+  std::vector<double> ud(1);
+  std::vector<SlotEnt> slot(32);
+  std::vector<uint8_t> slot_of(P.cat.M);
+  const LaneSmem S{nullptr, nullptr, slot.data(), prm.data(), ud.data(), wprm.data(), slot_of.data(), 1,
+                   nullptr, nullptr, nullptr};
+  if (g_xr)
+    replay_scenario<32, 8, D, true, true>(P, i, false, need_win && cap < P.cat.M, K, S, cap);
+  else
+    replay_scenario<32, 8, D, false, true>(P, i, false, need_win && cap < P.cat.M, K, S, cap);
 }
 
 extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -65,7 +84,7 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
                                      const int32_t* dump_slot, const int64_t* dump_off,
                                      uint8_t* cold, double* ttft, double* e2e, double* qw, double* lw,
                                      int64_t evict_cap, int32_t* evict_model, double* evict_clock,
-                                     int64_t* n_evict, int32_t xr) {
+                                     int64_t* n_evict, int32_t xr, int32_t wide) {
   g_xr = xr;
   try {
     HostCatalog cat;
@@ -96,7 +115,7 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
     P.dump.evict_model = evict_model;
     P.dump.evict_clock = evict_clock;
     P.dump.n_evict = n_evict;
-    if (cat.M > 64) return CACE_E_INVALID;
+    if (cat.M > 256) return CACE_E_INVALID;
     std::vector<float> p2f, tokf;
     for (int m = 0; m < cat.M; ++m) {
       p2f.push_back((float)cat.p2[m]);
@@ -114,6 +133,11 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
       }
       const int Cap = (int)effective_capacity(sc[i], cat.M);
       const bool D = dump_slot != nullptr;
+      if (wide || Cap > 16 || cat.M > 64) {  // the wide-pool lane kernel's code path
+        if (Cap > 32 || cat.M > 256) return CACE_E_INVALID;
+        D ? one_wide<true>(P, i, K, Cap) : one_wide<false>(P, i, K, Cap);
+        continue;
+      }
       switch (Cap) {
 #define CASE(k) case k: D ? one<k, true>(P, i, K) : one<k, false>(P, i, K); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)

@@ -113,3 +113,30 @@ def test_emulated_kernel_summaries_cfg_grid(ref, emul):
     want, _ = ref.run_batch(ref_catalog(ref, catalog), [ref_trace(t) for t in traces],
                             [ref_scenario(ref, s) for s in sc])
     assert_summaries_equal(got, want, "emulated grid")
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_emulated_wide_path_small_pools(ref, emul, seed):
+    """The wide-pool code path (runtime capacity, fp32 p2 + p4 formed on the
+    fly, exact p4 recomputed) forced on reference-expressible scenarios: full
+    per-request reports bit-exact against the reference."""
+    from paper_2506_18796_b200 import api, synth
+    from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig
+
+    rng = np.random.default_rng(4000 + seed)
+    catalog = synth.eight_model_catalog() if seed % 2 == 0 else api.ModelCatalog.build_default()
+    traces = [synth.mixed_trace(catalog, int(rng.integers(500, 3000)), seed=40 * seed + k,
+                                rate=float(rng.choice([1.0, 10.0, 40.0])), bursty=bool(k % 2)) for k in range(2)]
+    rows = []
+    for _ in range(30):
+        pol = PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.choice([0.0, 0.5, 1.0, 1.7])),
+                           window_length=int(rng.choice([1, 3, 10, 50])), p1_mode=int(rng.integers(0, 2)),
+                           output_token_normalizer=int(rng.choice([600, 50])))
+        rows.append((int(rng.integers(0, 2)), pol,
+                     ClusterConfig(num_accelerators=int(rng.integers(1, 16)),
+                                   unload_time_s=float(rng.choice([0.0, 0.5])))))
+    sc = api.make_scenarios(rows)
+    got, d = emul.replay_batch(traces, catalog, sc, _logv(), dump=True, wide=True)
+    rcat = ref_catalog(ref, catalog)
+    want, _ = ref.run_batch(rcat, [ref_trace(t) for t in traces], [ref_scenario(ref, s) for s in sc])
+    assert_summaries_equal(got, want, "wide path")

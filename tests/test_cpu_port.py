@@ -72,3 +72,28 @@ def test_emulated_kernel_large_pool_vs_port(port, n_models):
     got, _ = emul.replay_batch(traces, catalog, sc, api.probe_log_variant())
     want, _ = port.run_batch(port.Catalog(catalog), traces, sc)
     assert_summaries_equal(got, want, f"pool {n_models}")
+
+
+@pytest.mark.parametrize("n_models,cmax,window", [(100, 32, 40), (256, 32, 1024), (40, 24, 300)])
+def test_emulated_wide_pool_vs_port(port, n_models, cmax, window):
+    """The wide-pool lane path (pools up to 256 models, capacities up to 32;
+    BASELINE config 5 shape): host emulation vs the port oracle."""
+    from paper_2506_18796_b200 import api, synth
+    from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig
+    from tests import emul
+
+    rng = np.random.default_rng(n_models + cmax)
+    catalog = api.ModelCatalog.synthetic_pool(n_models, seed=n_models)
+    traces = [synth.mixed_trace(catalog, 4000, seed=k, rate=40.0, bursty=True) for k in range(2)]
+    rows = []
+    for _ in range(24):
+        pol = PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.choice([0.0, 0.5, 1.0, 1.7])),
+                           window_length=int(rng.choice([1, 10, window])), p1_mode=int(rng.integers(0, 2)),
+                           output_token_normalizer=catalog.max_expected_output_tokens())
+        rows.append((int(rng.integers(0, 2)), pol,
+                     ClusterConfig(num_accelerators=int(rng.integers(max(2, cmax // 2), cmax + 1)),
+                                   unload_time_s=float(rng.choice([0.0, 0.25])))))
+    sc = api.make_scenarios(rows)
+    got, _ = emul.replay_batch(traces, catalog, sc, api.probe_log_variant())
+    want, _ = port.run_batch(port.Catalog(catalog), traces, sc)
+    assert_summaries_equal(got, want, f"wide pool {n_models}")
