@@ -10,7 +10,7 @@
  *   cace_replay_batch        <- SimulationReport run(const Trace&, const ModelCatalog&,
  *                               const ClusterConfig&, const Policy&)      engine.hpp:60-61
  *                               + the scenario fan-out of run_grid          experiment.hpp:54-55
- *                                 (experiment.cpp:149-184, OpenMP over cells)
+ *                                 (experiment.cpp:87-122, OpenMP over cells)
  *   cace_select_victim_batch <- std::optional<std::string> select_victim(...) policy.hpp:67-71
  *   cace_eviction_score_batch<- ScoreBreakdown eviction_score(...)          policy.hpp:59-62
  *   cace_dedup_window_batch  <- LookaheadWindow dedup_window(...)           policy.hpp:56-57

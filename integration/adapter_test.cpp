@@ -55,7 +55,9 @@ int main() {
   all.p1_mode = P1Mode::Verbatim;
   for (auto* cfg : {&cmp, &abl, &all}) {
     const GridResult want = run_grid(*cfg, catalog, false);
-    const GridResult got = gpu::run_grid(*cfg, catalog);
+    const GridResult got = gpu::run_grid(*cfg, catalog, true);
+    const GridResult got_serial = gpu::run_grid(*cfg, catalog, false);
+    check(render(got) == render(got_serial), "run_grid parallel == serial (all visible devices vs device 0)");
     const std::string a = render(want), b = render(got);
     check(a == b, "run_grid byte-identical (" + std::to_string(a.size()) + " bytes, " +
                       std::to_string(cfg->patterns.size() * cfg->variants.size() * cfg->seeds.size()) +

@@ -7,6 +7,8 @@
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
+#include <string>
+#include <thread>
 
 #include "cace_gpu.h"
 #include "cacesim/metrics.hpp"
@@ -74,12 +76,39 @@ std::uint64_t config_hash(const ClusterConfig& cluster, const PolicyConfig& cfg)
   return fnv1a(ss.str());
 }
 
+// Runs [b, e) of the sweep on one device: a full dump (outcomes + eviction
+// log) straight into the caller's outcome columns (the runs' outcomes are
+// contiguous there, at off[b]).
+struct DumpCols {
+  std::vector<uint8_t> cold;
+  std::vector<double> qw, lw, pf, dc, tt, ee;
+  std::vector<int64_t> n_ev;
+  std::vector<cace_summary_t> summ;
+};
+
+void replay_range(int device, const CatalogSoA& cat, const std::vector<cace_trace_t>& tabi,
+                  const std::vector<cace_scenario_t>& sc, const std::vector<int64_t>& off, int64_t b,
+                  int64_t e, DumpCols& d, int32_t& rc, std::string& err) {
+  const int64_t n = e - b;
+  std::vector<int64_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  const int64_t o = off[b];
+  cace_dump_t dump{static_cast<int32_t>(n), idx.data(), d.cold.data() + o, d.qw.data() + o, d.lw.data() + o,
+                   d.pf.data() + o, d.dc.data() + o, d.tt.data() + o, d.ee.data() + o, 0, nullptr, nullptr,
+                   d.n_ev.data() + b};
+  cace_opts_t opts{device, CACE_KERNEL_AUTO, -1, 0, nullptr};
+  char msg[512] = {0};
+  rc = cace_replay_batch(&cat.abi, tabi.data(), static_cast<int32_t>(tabi.size()), sc.data() + b, n,
+                         d.summ.data() + b, &dump, &opts, msg, sizeof msg);
+  if (rc != CACE_OK) err = msg;
+}
+
 }  // namespace
 
 std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
                                        const ModelCatalog& catalog,
                                        const std::vector<std::pair<PolicyConfig, ClusterConfig>>& runs,
-                                       const std::vector<int>& trace_of_run) {
+                                       const std::vector<int>& trace_of_run, bool parallel) {
   // run() preconditions first, in the reference's order (engine.cpp:79-82),
   // then the per-request catalog lookups (engine.cpp:87-92).
   for (const auto& [pc, cc] : runs) {
@@ -94,22 +123,37 @@ std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
   const int64_t S = static_cast<int64_t>(runs.size());
   std::vector<cace_scenario_t> sc;
   for (int64_t i = 0; i < S; ++i) sc.push_back(scenario(trace_of_run[i], runs[i].first, runs[i].second));
-  // Full dump of every run: outcomes + eviction log.
-  std::vector<int64_t> idx(S), off(S + 1, 0);
-  std::iota(idx.begin(), idx.end(), 0);
+  std::vector<int64_t> off(S + 1, 0);
   for (int64_t i = 0; i < S; ++i) off[i + 1] = off[i] + tabi[trace_of_run[i]].n_requests;
   const int64_t total = off[S];
-  std::vector<uint8_t> cold(total);
-  std::vector<double> qw(total), lw(total), pf(total), dc(total), tt(total), ee(total);
-  std::vector<int64_t> n_ev(S);
-  cace_dump_t dump{static_cast<int32_t>(S), idx.data(), cold.data(), qw.data(), lw.data(), pf.data(),
-                   dc.data(), tt.data(), ee.data(), 0, nullptr, nullptr, n_ev.data()};
-  std::vector<cace_summary_t> summ(S);
-  cace_opts_t opts{0, CACE_KERNEL_AUTO, -1, 0, nullptr};
-  char msg[512] = {0};
-  const int32_t rc = cace_replay_batch(&cat.abi, tabi.data(), static_cast<int32_t>(tabi.size()),
-                                       sc.data(), S, summ.data(), &dump, &opts, msg, sizeof msg);
-  if (rc != CACE_OK) throw SimError(msg);  // same text as the reference's SimError
+  DumpCols d;
+  d.cold.resize(total);
+  for (auto* v : {&d.qw, &d.lw, &d.pf, &d.dc, &d.tt, &d.ee}) v->resize(total);
+  d.n_ev.resize(S);
+  d.summ.resize(S);
+  // The device-scale form of run_grid's OpenMP fan-out (experiment.cpp:100-115):
+  // with parallel and several GPUs, contiguous run ranges of about equal
+  // request count go to one host thread + device each; serial = device 0.
+  const int nd = parallel ? std::max(1, std::min<int>(cace_device_count(), static_cast<int>(S))) : 1;
+  std::vector<int64_t> cut(nd + 1, S);
+  cut[0] = 0;
+  for (int k = 1; k < nd; ++k)
+    cut[k] = std::lower_bound(off.begin(), off.end() - 1, total * k / nd) - off.begin();
+  std::vector<int32_t> rcs(nd, CACE_OK);
+  std::vector<std::string> errs(nd);
+  if (nd == 1) {
+    replay_range(0, cat, tabi, sc, off, 0, S, d, rcs[0], errs[0]);
+  } else {
+    std::vector<std::thread> th;
+    for (int k = 0; k < nd; ++k)
+      if (cut[k] < cut[k + 1])
+        th.emplace_back(replay_range, k, std::cref(cat), std::cref(tabi), std::cref(sc), std::cref(off),
+                        cut[k], cut[k + 1], std::ref(d), std::ref(rcs[k]), std::ref(errs[k]));
+    for (auto& t : th) t.join();
+  }
+  // the first failing run in sweep order wins, as the serial loop would raise it
+  for (int k = 0; k < nd; ++k)
+    if (rcs[k] != CACE_OK) throw SimError(errs[k]);  // same text as the reference's SimError
   std::vector<SimulationReport> out(S);
   for (int64_t i = 0; i < S; ++i) {
     const Trace& t = *traces[trace_of_run[i]];
@@ -119,12 +163,12 @@ std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
     rep.meta.seed = t.seed;
     rep.meta.pattern = t.pattern;
     rep.meta.config_hash = config_hash(cc, pc);
-    rep.counters.hits = summ[i].hits;
-    rep.counters.misses = summ[i].misses;
-    rep.counters.evictions = summ[i].evictions;
-    rep.counters.load_overhead_s = summ[i].load_overhead_s;
-    rep.loads = summ[i].loads;
-    rep.max_resident = summ[i].max_resident;
+    rep.counters.hits = d.summ[i].hits;
+    rep.counters.misses = d.summ[i].misses;
+    rep.counters.evictions = d.summ[i].evictions;
+    rep.counters.load_overhead_s = d.summ[i].load_overhead_s;
+    rep.loads = d.summ[i].loads;
+    rep.max_resident = d.summ[i].max_resident;
     rep.outcomes.resize(t.requests.size());
     for (size_t k = 0; k < t.requests.size(); ++k) {
       const int64_t o = off[i] + static_cast<int64_t>(k);
@@ -133,13 +177,13 @@ std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
       oc.request_id = r.request_id;
       oc.model_id = catalog.lookup(r.language, r.task_class).model_id;
       oc.task_class = r.task_class;
-      oc.cold_start = cold[o] != 0;
-      oc.queue_wait_s = qw[o];
-      oc.load_wait_s = lw[o];
-      oc.prefill_s = pf[o];
-      oc.decode_s = dc[o];
-      oc.ttft_s = tt[o];
-      oc.e2e_s = ee[o];
+      oc.cold_start = d.cold[o] != 0;
+      oc.queue_wait_s = d.qw[o];
+      oc.load_wait_s = d.lw[o];
+      oc.prefill_s = d.pf[o];
+      oc.decode_s = d.dc[o];
+      oc.ttft_s = d.tt[o];
+      oc.e2e_s = d.ee[o];
     }
   }
   return out;
@@ -147,13 +191,13 @@ std::vector<SimulationReport> run_many(const std::vector<const Trace*>& traces,
 
 SimulationReport run(const Trace& trace, const ModelCatalog& catalog, const ClusterConfig& cluster,
                      const Policy& policy) {
-  return run_many({&trace}, catalog, {{policy.config(), cluster}}, {0}).front();
+  return run_many({&trace}, catalog, {{policy.config(), cluster}}, {0}, false).front();
 }
 
 std::vector<RunMetrics> run_metrics_many(const std::vector<const Trace*>& traces,
                                          const ModelCatalog& catalog,
                                          const std::vector<std::pair<PolicyConfig, ClusterConfig>>& runs,
-                                         const std::vector<int>& trace_of_run) {
+                                         const std::vector<int>& trace_of_run, bool parallel) {
   for (const auto& [pc, cc] : runs) {  // engine.cpp:79-82, in the reference's order
     if (pc.window_length < 1) throw SimError("run: window_length must be >= 1");
     if (cc.num_accelerators < 1) throw SimError("run: need at least one accelerator");
@@ -167,11 +211,34 @@ std::vector<RunMetrics> run_metrics_many(const std::vector<const Trace*>& traces
   std::vector<cace_scenario_t> sc;
   for (int64_t i = 0; i < S; ++i) sc.push_back(scenario(trace_of_run[i], runs[i].first, runs[i].second));
   std::vector<cace_run_metrics_t> m(S);
-  cace_opts_t opts{0, CACE_KERNEL_AUTO, -1, 0, nullptr};
-  char msg[512] = {0};
-  const int32_t rc = cace_run_metrics_batch(&cat.abi, tabi.data(), static_cast<int32_t>(tabi.size()),
-                                            sc.data(), S, m.data(), nullptr, &opts, msg, sizeof msg);
-  if (rc != CACE_OK) throw SimError(msg);
+  // same device fan-out as run_many, cut by request count
+  std::vector<int64_t> off(S + 1, 0);
+  for (int64_t i = 0; i < S; ++i) off[i + 1] = off[i] + tabi[trace_of_run[i]].n_requests;
+  const int nd = parallel ? std::max(1, std::min<int>(cace_device_count(), static_cast<int>(S))) : 1;
+  std::vector<int64_t> cut(nd + 1, S);
+  cut[0] = 0;
+  for (int k = 1; k < nd; ++k)
+    cut[k] = std::lower_bound(off.begin(), off.end() - 1, off[S] * k / nd) - off.begin();
+  std::vector<int32_t> rcs(nd, CACE_OK);
+  std::vector<std::string> errs(nd);
+  auto part = [&](int k) {
+    const int64_t b = cut[k], n = cut[k + 1] - cut[k];
+    if (n == 0) return;
+    cace_opts_t opts{k, CACE_KERNEL_AUTO, -1, 0, nullptr};
+    char msg[512] = {0};
+    rcs[k] = cace_run_metrics_batch(&cat.abi, tabi.data(), static_cast<int32_t>(tabi.size()), sc.data() + b, n,
+                                    m.data() + b, nullptr, &opts, msg, sizeof msg);
+    if (rcs[k] != CACE_OK) errs[k] = msg;
+  };
+  if (nd == 1) {
+    part(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int k = 0; k < nd; ++k) th.emplace_back(part, k);
+    for (auto& t : th) t.join();
+  }
+  for (int k = 0; k < nd; ++k)
+    if (rcs[k] != CACE_OK) throw SimError(errs[k]);
   std::vector<RunMetrics> out(S);
   for (int64_t i = 0; i < S; ++i) {
     RunMetrics& r = out[i];
@@ -192,7 +259,7 @@ std::vector<RunMetrics> run_metrics_many(const std::vector<const Trace*>& traces
   return out;
 }
 
-GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& catalog) {
+GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& catalog, bool parallel) {
   cfg.validate();
   std::vector<Trace> traces;
   std::vector<const Trace*> tp;
@@ -209,7 +276,7 @@ GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& cat
         runs.emplace_back(make_policy_config(cfg, v, catalog), cfg.cluster);
         tof.push_back(static_cast<int>(pi) * ns + si);
       }
-  std::vector<RunMetrics> ms = run_metrics_many(tp, catalog, runs, tof);
+  std::vector<RunMetrics> ms = run_metrics_many(tp, catalog, runs, tof, parallel);
   GridResult result;
   size_t r = 0;
   for (size_t pi = 0; pi < cfg.patterns.size(); ++pi)
@@ -234,7 +301,7 @@ GridResult run_grid_metrics(const ExperimentConfig& cfg, const ModelCatalog& cat
   return result;
 }
 
-GridResult run_grid(const ExperimentConfig& cfg, const ModelCatalog& catalog) {
+GridResult run_grid(const ExperimentConfig& cfg, const ModelCatalog& catalog, bool parallel) {
   cfg.validate();
   // Traces per (pattern, seed), exactly as run_cell builds them (experiment.cpp:74-80).
   std::vector<Trace> traces;
@@ -252,7 +319,7 @@ GridResult run_grid(const ExperimentConfig& cfg, const ModelCatalog& catalog) {
         runs.emplace_back(make_policy_config(cfg, v, catalog), cfg.cluster);
         tof.push_back(static_cast<int>(pi) * ns + si);
       }
-  std::vector<SimulationReport> reps = run_many(tp, catalog, runs, tof);
+  std::vector<SimulationReport> reps = run_many(tp, catalog, runs, tof, parallel);
   GridResult result;
   size_t r = 0;
   for (PatternName p : cfg.patterns)

@@ -8,7 +8,7 @@
 // catalog.hpp:45-58 ModelCatalog) and converts plain arrays to/from its types.
 //
 // The reference does not expose its eviction sequence, so the link step wraps
-// the one external call engine.cpp:269 makes into policy.cpp
+// the one external call engine.cpp:203 makes into policy.cpp
 // (`-Wl,--wrap=<cacesim::select_victim>`, see Makefile): every non-empty victim
 // returned to run() is appended to a thread-local recorder.  The reference code
 // itself is untouched.

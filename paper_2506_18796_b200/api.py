@@ -8,7 +8,7 @@ Names, argument meaning and error behaviour follow the reference
 * ``PolicyConfig`` / ``Variant`` / ``P1Mode``   policy.hpp:29-45, types.hpp:63-70
 * ``ClusterConfig``   engine.hpp:13-17
 * ``run()`` -> ``SimulationReport``   engine.hpp:60-61 (one scenario, full outcomes)
-* ``run_batch()``   the scenario fan-out of ``run_grid`` (experiment.cpp:149-184),
+* ``run_batch()``   the scenario fan-out of ``run_grid`` (experiment.cpp:87-122),
   one fixed-size summary per scenario
 * ``select_victim`` / ``eviction_score`` / ``dedup_window`` / ``service_times``
   policy.hpp:56-71, engine.hpp:54-55 (batched)
@@ -71,7 +71,7 @@ class Variant(enum.IntEnum):  # types.hpp:63-70
 VARIANT_NAMES = ["lru", "cace", "cace-p1", "cace-p2", "cace-p3", "cace-p4"]
 
 
-def variant_from_string(s: str) -> Variant:  # types.cpp:716-724
+def variant_from_string(s: str) -> Variant:  # types.cpp:69-77
     if s not in VARIANT_NAMES:
         raise SimError("unknown policy variant: " + s)
     return Variant(VARIANT_NAMES.index(s))
