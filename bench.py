@@ -443,6 +443,8 @@ def main():
             parity = {"scenarios": int(len(pidx)), "bit_exact": bool(ok),
                       "sample": "stratified over (capacity, variant, P1 mode, window); every summary field incl. "
                                 "the outcome and eviction-sequence fingerprints", "cpu_seconds": psecs}
+            if args.cpu_sample <= 0:
+                raise RuntimeError("--cpu-sample 0: CPU baseline not timed")
             cidx = np.sort(np.random.default_rng(777).choice(len(sc_all), size=min(args.cpu_sample, len(sc_all)),
                                                              replace=False))
             _, secs, kind = cpu_run(catalog, traces, sc_all, cidx, threads, summaries=False)

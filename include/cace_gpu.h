@@ -257,7 +257,9 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
  * {p50, p95, p99, max}[j]; an empty class yields zeros (the caller reports
  * the reference's SimError).  spec: 1 speculative first digit (default
  * pipeline behaviour), 0 off, 2 every speculation forced to miss (test hook).
- * Host memory; the samples are copied (the kernel compacts its copy). */
+ * Host memory; the samples are copied (the kernel compacts its copy
+ * segment by segment in place, so segments must be disjoint: overlapping
+ * [off, off + nreq) ranges are rejected with CACE_E_INVALID). */
 int32_t cace_metrics_select(const double* samples, const int64_t* off, const uint32_t* ncomp,
                             const uint32_t* nreq, int64_t n_segments, double* stat, int32_t spec,
                             const cace_opts_t* opts, char* msg, size_t msg_cap);

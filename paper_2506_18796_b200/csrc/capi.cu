@@ -976,9 +976,20 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     }
     const int64_t NL = (int64_t)loc_scen.size();
     pt.mark("chunks");
+    // A 32-scenario unit larger than budget / W still forms its own chunk,
+    // so the rings are a soft budget: use only as many rings as the largest
+    // chunk allows inside the budget (fewer rings, less overlap), and fail
+    // early when one chunk alone does not fit the free memory.
+    int64_t max_chunk = 1;
+    for (const auto& c : chunks) max_chunk = std::max(max_chunk, c.nsamp);
+    if ((size_t)max_chunk * 8 > free_b)
+      throw Invalid{CACE_E_INVALID, "cace: run_metrics: one warp of scenarios needs " +
+                                        std::to_string((size_t)max_chunk * 8 >> 20) +
+                                        " MB of samples, more than the free device memory"};
+    const size_t WR = std::max<size_t>(1, std::min<size_t>(W, budget / ((size_t)max_chunk * 8)));
     std::vector<int64_t> ring_len(W, 0);
     for (size_t j = 0; j < chunks.size(); ++j)
-      ring_len[j % W] = std::max(ring_len[j % W], chunks[j].nsamp);
+      ring_len[j % WR] = std::max(ring_len[j % WR], chunks[j].nsamp);
     DBuf<cace_scenario_t> d_sc;
     d_sc.upload(scenarios, n_scenarios, s);
     DBuf<cace_summary_t> d_out;
@@ -1014,7 +1025,7 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     } ss;
     int prio_lo = 0, prio_hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    const size_t nring = std::min(W, chunks.size());
+    const size_t nring = std::min(WR, chunks.size());
     for (size_t r = 0; r < nring; ++r) {
       cudaStream_t x;
       cudaEvent_t a, b;
@@ -1039,9 +1050,9 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     fork_workers(e, s, chunks.size());
     for (size_t j = 0; j < chunks.size(); ++j) {
       const Chunk& c = chunks[j];
-      const size_t r = j % W;
+      const size_t r = j % WR;
       cudaStream_t ws = e->workers[r];
-      if (j >= W) CK(cudaStreamWaitEvent(ws, ss.sel[r], 0));  // ring r is free again
+      if (j >= WR) CK(cudaStreamWaitEvent(ws, ss.sel[r], 0));  // ring r is free again
       if (pt.on) CK(cudaEventRecord(tl[3 * j], ws));
       ReplayParams P = P0;
       P.dump.dump_off = d_off.p + c.base;
@@ -1145,6 +1156,15 @@ int32_t cace_metrics_select(const double* samples, const int64_t* off, const uin
     for (int64_t b = 0; b < n_segments; ++b) {
       if (ncomp[b] > nreq[b] || off[b] < 0) throw Invalid{CACE_E_INVALID, "cace: bad segment"};
       total = std::max<int64_t>(total, off[b] + (int64_t)nreq[b]);
+    }
+    {
+      // the select compacts each segment in place: segments must not overlap
+      std::vector<int64_t> ord(n_segments);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return off[a] < off[b]; });
+      for (int64_t q = 1; q < n_segments; ++q)
+        if (nreq[ord[q - 1]] > 0 && nreq[ord[q]] > 0 && off[ord[q - 1]] + (int64_t)nreq[ord[q - 1]] > off[ord[q]])
+          throw Invalid{CACE_E_INVALID, "cace: overlapping sample segments"};
     }
     cudaStream_t s = opts && opts->stream ? static_cast<cudaStream_t>(opts->stream) : nullptr;
     DBuf<double> d_samp, d_stat;

@@ -61,6 +61,12 @@
 #include "glibc_log.cuh"
 #include "replay_types.h"
 
+// Instrumentation hook of the test-only host emulation (per-request decision
+// statistics, tools/decision_stats.py); compiled out of the product.
+#ifndef CACE_STAT
+#define CACE_STAT(kind, k)
+#endif
+
 namespace cace {
 
 // Summary fingerprint (spec CACE_HASH in include/cace_gpu.h).
@@ -500,6 +506,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const bool hit = hs >= 0;
     if (hit) {
       ++hits;
+      CACE_STAT(0, k);
       // Busy: blocked until the model's own ServiceComplete (td, 1, tq)
       // (engine.cpp:175-181); every earlier completion just idles its slot.
       const double td = S.slot[hs * st].done;
@@ -514,6 +521,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (occ < cap) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
       } else {
+        CACE_STAT(1, k);
         if constexpr (!WIDE) {
         // Full: the Idle residents are the eviction candidates
         // (engine.cpp:189-208, policy.cpp:85-89).
@@ -549,11 +557,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           ct = t1;
           cw = kKindSC | q1;
           v = s1;
+          CACE_STAT(2, k);
         } else if ((idm & (idm - 1u)) == 0) {
           v = __ffs(idm) - 1;  // exactly one candidate
+          CACE_STAT(3, k);
         } else {
           // ---- eviction decision among >= 2 idle residents ----------
           const double now = ct;
+          CACE_STAT(4, k);
           if (is_lru) {
             // sorted-first = min (last_used, lex) over idle (policy.cpp:92-100)
             int f = -1;
@@ -608,6 +619,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             }
             v = bs;
             if (!(best - second > S.prm[3 * st])) {
+              CACE_STAT(5, k);
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
               // strict max in (last_used, model_id) order"
               // (policy.cpp:92-113), bit-identical to the reference; taken on

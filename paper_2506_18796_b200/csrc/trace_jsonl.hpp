@@ -127,6 +127,33 @@ struct Parser {
       const unsigned char c = (unsigned char)*p++;
       if (c == '"') break;
       if (c < 0x20) fail("control character in string");
+      if (c >= 0x80) {  // well-formed UTF-8 only (RFC 3629 ranges, as nlohmann's scan_string)
+        int more;
+        unsigned char lo = 0x80, hi = 0xBF;
+        if (c >= 0xC2 && c <= 0xDF) {
+          more = 1;
+        } else if (c >= 0xE0 && c <= 0xEF) {
+          more = 2;
+          if (c == 0xE0) lo = 0xA0;
+          if (c == 0xED) hi = 0x9F;
+        } else if (c >= 0xF0 && c <= 0xF4) {
+          more = 3;
+          if (c == 0xF0) lo = 0x90;
+          if (c == 0xF4) hi = 0x8F;
+        } else {
+          fail("ill-formed UTF-8 byte");
+        }
+        out += (char)c;
+        for (int q = 0; q < more; ++q) {
+          if (p >= e) fail("ill-formed UTF-8 byte");
+          const unsigned char d = (unsigned char)*p++;
+          if (d < lo || d > hi) fail("ill-formed UTF-8 byte");
+          out += (char)d;
+          lo = 0x80;
+          hi = 0xBF;
+        }
+        continue;
+      }
       if (c != '\\') {
         out += (char)c;
         continue;
@@ -213,50 +240,49 @@ struct Parser {
     if (!std::isfinite(v.d))  // nlohmann rejects overflowing literals (lexer, out_of_range.406)
       throw LineError{"[json.exception.out_of_range.406] number overflow parsing '" + tok + "'"};
   }
-  void skip_value(int depth) {
-    if (depth > 512) fail("nesting too deep");
-    ws();
-    if (p >= e) fail("unexpected end of input");
-    if (*p == '{') {
-      ++p;
+  // Skips one value of any nesting depth with an explicit stack (nlohmann's
+  // parser is iterative and has no depth limit).
+  void skip_value() {
+    std::vector<char> open;  // '{' / '[' of the containers being skipped
+    while (true) {
       ws();
-      if (p < e && *p == '}') {
-        ++p;
-        return;
+      if (p >= e) fail("unexpected end of input");
+      if (*p == '{' || *p == '[') {
+        const char c = *p++;
+        ws();
+        if (p < e && *p == (c == '{' ? '}' : ']')) {
+          ++p;
+        } else {
+          open.push_back(c);
+          if (c == '{') {
+            (void)str();
+            expect(':', "expected ':'");
+          }
+          continue;  // the container's first value
+        }
+      } else {
+        Val v;
+        scalar(v);
       }
+      // a value ended: continue or close its containers
       while (true) {
-        (void)str();
-        expect(':', "expected ':'");
-        skip_value(depth + 1);
+        if (open.empty()) return;
         ws();
         if (p < e && *p == ',') {
           ++p;
-          continue;
+          if (open.back() == '{') {
+            (void)str();
+            expect(':', "expected ':'");
+          }
+          break;
         }
-        expect('}', "expected ',' or '}'");
-        return;
+        if (open.back() == '{')
+          expect('}', "expected ',' or '}'");
+        else
+          expect(']', "expected ',' or ']'");
+        open.pop_back();
       }
     }
-    if (*p == '[') {
-      ++p;
-      ws();
-      if (p < e && *p == ']') {
-        ++p;
-        return;
-      }
-      while (true) {
-        skip_value(depth + 1);
-        ws();
-        if (p < e && *p == ',') {
-          ++p;
-          continue;
-        }
-        expect(']', "expected ',' or ']'");
-        return;
-      }
-    }
-    Val v;
-    scalar(v);
   }
   void literal(const char* w) {
     const size_t n = std::strlen(w);
@@ -294,12 +320,19 @@ struct Parser {
   Kind top = K_NONE;  // kind of the document when it is not an object
   template <class F>
   bool object(F&& on_field) {
+    // a UTF-8 byte order mark at the start of the document is skipped, as
+    // nlohmann's lexer does (skip_bom); a partial one is a syntax error
+    if (p < e && (unsigned char)*p == 0xEF) {
+      if (e - p < 3 || (unsigned char)p[1] != 0xBB || (unsigned char)p[2] != 0xBF)
+        fail("invalid BOM; must be 0xEF 0xBB 0xBF if given");
+      p += 3;
+    }
     ws();
     if (p >= e) fail("unexpected end of input");
     if (*p != '{') {
       const char c = *p;
       top = c == '[' ? K_ARRAY : c == '"' ? K_STRING : (c == 't' || c == 'f') ? K_BOOL : c == 'n' ? K_NULL : K_UINT;
-      skip_value(0);
+      skip_value();
       ws();
       if (p != e) fail("trailing characters");
       return false;
@@ -316,7 +349,7 @@ struct Parser {
         Val v;
         if (p < e && (*p == '{' || *p == '[')) {
           v.kind = *p == '{' ? K_OBJECT : K_ARRAY;
-          skip_value(1);
+          skip_value();
         } else {
           scalar(v);
         }

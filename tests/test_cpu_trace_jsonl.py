@@ -213,3 +213,28 @@ def test_fuzz_against_reference(ref):
             else:
                 assert got == err, (case, err, got)
     assert mutations > 300
+
+
+def test_bom_utf8_and_deep_nesting(ref):
+    """Advisor round 1: a UTF-8 BOM at the start of a line is skipped (nlohmann
+    skip_bom), a partial BOM is an error, ill-formed UTF-8 inside a string is
+    an error (parse_error.101), well-formed multi-byte UTF-8 passes, and an
+    ignored field may nest deeper than 512 (nlohmann's parser has no limit)."""
+    bom = b"\xef\xbb\xbf"
+    _same(ref, bom + HDR + _rec(0, 0.5) + _rec(1, 1.0))
+    _same(ref, HDR + bom + _rec(0, 0.5) + _rec(1, 1.0))
+    _err(ref, b"\xef\xbb" + HDR + _rec(0, 0.5), prefix_only=True)
+    good = ['"\xc3\xa9"', '"\xe2\x82\xac"', '"\xf0\x9f\x98\x80"', '"\xed\x9f\xbf"', '"\xf4\x8f\xbf\xbf"']
+    for g in good:
+        line = _rec(0, 0.5)[:-2] + b',"note":' + g.encode("latin-1") + b"}\n"
+        _same(ref, HDR + line)
+    bad = [b'"\x80"', b'"\xc0\xaf"', b'"\xc3"', b'"\xe0\x80\x80"', b'"\xed\xa0\x80"', b'"\xf0\x80\x80\x80"',
+           b'"\xf4\x90\x80\x80"', b'"\xf5\x80\x80\x80"', b'"\xe2\x82"']
+    for b_ in bad:
+        line = _rec(0, 0.5)[:-2] + b',"note":' + b_ + b"}\n"
+        _err(ref, HDR + line, prefix_only=True)
+    deep = b"[" * 3000 + b"]" * 3000
+    _same(ref, HDR + _rec(0, 0.5)[:-2] + b',"deep":' + deep + b"}\n")
+    deep_obj = b'{"a":' * 1500 + b"1" + b"}" * 1500
+    _same(ref, HDR + _rec(0, 0.5)[:-2] + b',"deep":' + deep_obj + b"}\n")
+    _err(ref, HDR + _rec(0, 0.5)[:-2] + b',"deep":' + b"[" * 700 + b"]" * 699 + b"}\n", prefix_only=True)

@@ -78,9 +78,10 @@ def test_run_metrics_config4_slice(ref):
 
 
 def test_run_metrics_chunked_pipeline(ref, monkeypatch):
-    """A tiny sample budget cuts the sweep into one-warp chunks over the ring
-    buffers (cace_run_metrics_batch's pipeline): same records as one chunk
-    per segment, and bit-exact against the reference."""
+    """A tiny sample budget cuts the sweep into one-warp chunks (cace_run_metrics_batch's
+    pipeline); a one-warp chunk (5 MB) exceeds the 1 MB budget, so the pipeline
+    falls back to a single ring instead of allocating all 8 (advisor round 1):
+    same records as one chunk per segment, and bit-exact against the reference."""
     catalog = synth.eight_model_catalog()
     traces = [synth.mixed_trace(catalog, 20_000, seed=7 + s) for s in range(2)]
     sc = synth.scenario_grid(synth.weight_vectors_cfg3()[::211], range(1, 9), 2,
@@ -207,3 +208,24 @@ def test_metrics_select_kernel_edges(spec):
         for c, x in enumerate((a, b)):
             want = _nearest_rank_stats(x)
             assert np.array_equal(bits(got[i, c]), bits(want)), (i, c, len(x), got[i, c], want)
+
+
+@pytest.mark.gpu
+def test_metrics_select_rejects_overlapping_segments():
+    """The select compacts each segment in place, so the C ABI rejects
+    overlapping sample ranges instead of racing (advisor round 1)."""
+    import ctypes as C
+
+    from paper_2506_18796_b200 import _native as N
+
+    flat = np.arange(10, dtype=np.float64)
+    off = np.array([0, 4], np.int64)
+    ncomp = np.array([3, 3], np.uint32)
+    stat = np.zeros(16)
+    msg = C.create_string_buffer(256)
+    opts = N.OptsABI(0, 0, -1, 0, None)
+    for nreq, want in ((np.array([4, 6], np.uint32), N.CACE_OK), (np.array([5, 6], np.uint32), N.CACE_E_INVALID)):
+        rc = N.lib.cace_metrics_select(N.ptr(flat), N.ptr(off), N.ptr(ncomp), N.ptr(nreq), 2, N.ptr(stat), 1,
+                                       C.byref(opts), msg, len(msg))
+        assert rc == want, (rc, msg.value)
+    assert b"overlapping" in msg.value

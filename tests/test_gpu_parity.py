@@ -5,6 +5,8 @@ cache-hit decisions bit-exact; TTFT/E2E within 1e-9 relative in fp64 — we
 assert the stronger bit-exact equality (tolerance 0) on every per-request
 field.  Sizes are chosen so the oracle finishes in seconds.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -44,6 +46,37 @@ def test_device_log_bit_exact_vs_libm(ref):
     want = ref.libm_log(x)
     bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))[0]
     assert len(bad) == 0, f"{len(bad)} mismatches, e.g. x={x[bad[:4]]}"
+
+
+def test_device_log_sweep_1e9_vs_libm(ref):
+    """SURVEY section 7 hard part 1: >= 10^9 inputs of the device glibc-log
+    restatement against this box's libm, bit for bit.  20 chunks of 5e7:
+    chunk 0 dense over the near-1 polynomial path [1 - 2^-4, 1 + 0x1.09p-4),
+    the rest uniform 52-bit mantissas at every exponent of t = clock -
+    last_used in [1, 2^44) -- all 128 table buckets at every exponent.  The
+    host libm runs on all cores (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(2026)
+    per, chunks, threads = 50_000_000, 20, os.cpu_count() or 4
+    total = bad = 0
+    seen = np.zeros((44, 128), bool)
+    with ThreadPoolExecutor(threads) as pool:
+        for c in range(chunks):
+            if c == 0:
+                x = rng.uniform(1.0 - 2.0**-4, 1.0 + 0x109 / 2.0**12, per)
+            else:
+                e = rng.integers(1023, 1023 + 44, per, dtype=np.uint64)
+                mant = rng.integers(0, 1 << 52, per, dtype=np.uint64)
+                x = ((e << np.uint64(52)) | mant).view(np.float64)
+                seen[(e - 1023).astype(np.int64), (mant >> np.uint64(45)).astype(np.int64)] = True
+            got = api.device_log(x)
+            parts = np.array_split(x, threads)
+            want = np.concatenate(list(pool.map(ref.libm_log, parts)))
+            bad += int(np.count_nonzero(got.view(np.uint64) != want.view(np.uint64)))
+            total += len(x)
+    assert total >= 1_000_000_000 and seen.all()
+    assert bad == 0, f"{bad} mismatches in {total} inputs"
 
 
 def test_config2_cace_vs_lru_bit_exact(ref):
