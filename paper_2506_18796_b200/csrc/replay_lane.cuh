@@ -253,14 +253,19 @@ struct Window {
 };
 
 // Trace records of the warp's trace in replay order.  Device: per-warp
-// shared-memory double buffer of 2 x 32 records filled by cp.async one chunk
-// ahead (collective: every lane copies one record per chunk).
+// shared-memory double buffer of 2 x 32 records, filled one chunk ahead.
+// Default: ONE bulk copy per chunk (cp.async.bulk on the TMA engine; SASS
+// UBLKCP) issued by lane 0 and completed on a per-buffer mbarrier
+// (expect_tx / complete_tx) that the warp waits on with try_wait.parity.
+// CACE_REC_LDGSTS selects round 1's per-lane cp.async staging (LDGSTS,
+// 3 x 16 B per lane) for A/B measurements.
 struct RecStream {
 #ifdef CACE_HOST_EMULATION
   const ReqRec* g;
-  void init(const ReqRec* g_, uint32_t, ReqRec*) { g = g_; }
+  void init(const ReqRec* g_, uint32_t, ReqRec*, uint64_t*) { g = g_; }
+  void fini() {}
   const ReqRec* chunk(uint32_t c) { return g + (size_t)c * 32; }
-#else
+#elif defined(CACE_REC_LDGSTS)
   const ReqRec* g;
   uint32_t n;
   ReqRec* buf;
@@ -277,16 +282,74 @@ struct RecStream {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  __device__ __forceinline__ void init(const ReqRec* g_, uint32_t n_, ReqRec* buf_) {
+  __device__ __forceinline__ void init(const ReqRec* g_, uint32_t n_, ReqRec* buf_, uint64_t*) {
     g = g_;
     n = n_;
     buf = buf_;
     issue(0);
   }
+  __device__ __forceinline__ void fini() { __syncwarp(); }
   // Collective: records [32c, 32c + 32) once chunk c has landed; prefetches
   // chunk c + 1 into the other half.
   __device__ __forceinline__ const ReqRec* chunk(uint32_t c) {
     asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    issue(c + 1);
+    return buf + (c & 1) * 32;
+  }
+#else
+  const ReqRec* g;
+  uint32_t n;
+  ReqRec* buf;
+  uint32_t bar;  // shared address of the two mbarriers (8 B each)
+  __device__ __forceinline__ void issue(uint32_t c) {
+    if ((threadIdx.x & 31) == 0 && c * 32 < n) {
+      const uint32_t bytes = min(32u, n - c * 32) * (uint32_t)sizeof(ReqRec);  // multiple of 16
+      const uint32_t b = bar + (c & 1) * 8;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + (c & 1) * 32);
+      // the warp's generic-proxy reads of this half (chunk c - 2) precede the
+      // async-proxy write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(g + (size_t)c * 32), "r"(bytes), "r"(b)
+                   : "memory");
+    }
+  }
+  __device__ __forceinline__ void init(const ReqRec* g_, uint32_t n_, ReqRec* buf_, uint64_t* bar_) {
+    g = g_;
+    n = n_;
+    buf = buf_;
+    bar = (uint32_t)__cvta_generic_to_shared(bar_);
+    if ((threadIdx.x & 31) == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue(0);
+  }
+  // Collective, after the last chunk: no copy is in flight; the barriers are
+  // invalidated so the memory can be re-initialised for the warp's next replay.
+  __device__ __forceinline__ void fini() {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar + 8) : "memory");
+    }
+    __syncwarp();
+  }
+  // Collective: records [32c, 32c + 32) once chunk c has landed (phase c / 2
+  // of its half's mbarrier); prefetches chunk c + 1 into the other half.
+  __device__ __forceinline__ const ReqRec* chunk(uint32_t c) {
+    const uint32_t b = bar + (c & 1) * 8, par = (c >> 1) & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(b), "r"(par)
+          : "memory");
     __syncwarp();
     issue(c + 1);
     return buf + (c & 1) * 32;
@@ -327,6 +390,7 @@ struct LaneSmem {
   ReqRec* rec;       // warp: record double buffer [64]
   WinEnt* win;       // warp: window table [M]
   double* samp;      // warp: metrics sample tile [2 classes][kSampT][32 lanes] (DUMP only)
+  uint64_t* rbar;    // warp: the record buffers' two mbarriers
 };
 
 // Event cursor (time, kind, seq) of engine.cpp:49-55 as (ct, cw) with
@@ -463,7 +527,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   }
 #endif
   RecStream rs;
-  rs.init(tr, n, S.rec);
+  rs.init(tr, n, S.rec, S.rbar);
   Window<MW> win;
   if (C > 1 && warp_win) win.init(P.first0 + (int64_t)sc.trace * M, M, tr, n, S.win);
 
@@ -509,8 +573,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       CACE_STAT(0, k);
       // Busy: blocked until the model's own ServiceComplete (td, 1, tq)
       // (engine.cpp:175-181); every earlier completion just idles its slot.
-      const double td = S.slot[hs * st].done;
-      const uint32_t tq = S.slot[hs * st].seq;
+      const SlotEnt te = S.slot[hs * st];  // one 16-B load
+      const double td = te.done;
+      const uint32_t tq = te.seq;
       if (!sc_popped(td, tq, ct, cw)) {
         ct = td;
         cw = kKindSC | tq;
@@ -876,8 +941,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const double ttft = qd + pf;
     const double e2e = ttft + dc;
     const double done = (now + pf) + dc;
-    S.slot[hs * st].done = done;
-    S.slot[hs * st].seq = k;
+    {
+      SlotEnt* const sp = &S.slot[hs * st];  // one address for both stores
+      sp->done = done;
+      sp->seq = k;
+    }
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
       mttft = ttft > mttft ? ttft : mttft;
@@ -925,6 +993,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   }
   }
 
+  rs.fini();
 #ifndef CACE_HOST_EMULATION
   if (DM == 2 || (DM == 1 && P.dump.samples)) {  // partial tiles
     const uint32_t nco = samp_ncomp(S.samp), nre = n - nco;
@@ -974,7 +1043,9 @@ inline __host__ __device__ size_t lane_smem_lane(int M, int C) {
   return (size_t)LANE_BLOCK * ((M + 1) * 8 + C * sizeof(SlotEnt) + M * 4 + 4 * 4 + M);
 }
 inline __host__ __device__ size_t lane_smem_warp(int M, bool dump) {
-  return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + (dump ? (2 * kSampT * 32 + 32 + 2) * sizeof(double) : 0);  // 16-B multiple: keeps the next warp's records aligned
+  // records, window table, 2 mbarriers, sample tile: a 16-B multiple keeps the next warp's records aligned
+  return 64 * sizeof(ReqRec) + (size_t)M * sizeof(WinEnt) + 16 +
+         (dump ? (2 * kSampT * 32 + 32 + 2) * sizeof(double) : 0);
 }
 inline size_t lane_smem_bytes(int M, int C, bool dump) {
   const size_t a = (lane_smem_lane_off(M) + lane_smem_lane(M, C) + 15) & ~(size_t)15;
@@ -1011,7 +1082,8 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
                          (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
   ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
   WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
-  double* w_samp = reinterpret_cast<double*>(w_win + M);
+  uint64_t* w_bar = reinterpret_cast<uint64_t*>(w_win + M);
+  double* w_samp = reinterpret_cast<double*>(w_bar + 2);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
@@ -1034,7 +1106,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_slot + threadIdx.x, l_prm + threadIdx.x,
                    l_p4d + (size_t)M * LANE_BLOCK + threadIdx.x, nullptr, l_sof + threadIdx.x, LANE_BLOCK,
-                   w_rec, w_win, w_samp};
+                   w_rec, w_win, w_samp, w_bar};
   replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
 }
 
@@ -1079,7 +1151,8 @@ __global__ void __launch_bounds__(LANE_BLOCK_WIDE, 4) replay_lane_wide_kernel(Re
                          (size_t)(threadIdx.x >> 5) * lane_smem_warp(M, DM != 0);
   ReqRec* w_rec = reinterpret_cast<ReqRec*>(wbase);
   WinEnt* w_win = reinterpret_cast<WinEnt*>(w_rec + 64);
-  double* w_samp = reinterpret_cast<double*>(w_win + M);
+  uint64_t* w_bar = reinterpret_cast<uint64_t*>(w_win + M);
+  double* w_samp = reinterpret_cast<double*>(w_bar + 2);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     s_lt[m] = P.cat.load_time[m];
     s_p2[m] = P.cat.p2[m];
@@ -1104,7 +1177,7 @@ __global__ void __launch_bounds__(LANE_BLOCK_WIDE, 4) replay_lane_wide_kernel(Re
   const bool warp_win = __any_sync(kFull, need_win) && cap < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{nullptr, nullptr, l_slot + col, l_prm + col, l_ud + col, l_wprm + col, l_sof + col, SB,
-                   w_rec, w_win, w_samp};
+                   w_rec, w_win, w_samp, w_bar};
   replay_scenario<C, MW, DM, true, true, G>(P, sidx, shadow, warp_win, K, S, cap);
 }
 #endif  // CACE_HOST_EMULATION

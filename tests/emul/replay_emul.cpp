@@ -54,7 +54,7 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
   std::vector<SlotEnt> slot(C);
   std::vector<uint8_t> slot_of(P.cat.M);
   const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), p4d.data() + P.cat.M, nullptr, slot_of.data(),
-                   1, nullptr, nullptr, nullptr};
+                   1, nullptr, nullptr, nullptr, nullptr};
   if (g_xr)
     replay_scenario<C, 2, D, true>(P, i, false, need_win, K, S);
   else
@@ -71,7 +71,7 @@ static void one_wide(const ReplayParams& P, int64_t i, const CatShared& K, int c
   std::vector<SlotEnt> slot(32);
   std::vector<uint8_t> slot_of(P.cat.M);
   const LaneSmem S{nullptr, nullptr, slot.data(), prm.data(), ud.data(), wprm.data(), slot_of.data(), 1,
-                   nullptr, nullptr, nullptr};
+                   nullptr, nullptr, nullptr, nullptr};
   if (g_xr)
     replay_scenario<32, 8, D, true, true>(P, i, false, need_win && cap < P.cat.M, K, S, cap);
   else

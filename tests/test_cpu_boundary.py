@@ -159,3 +159,19 @@ def test_multiprocess_shard_gather_gloo(ref, tmp_path):
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "GATHER_OK" in out.stdout
+
+
+def test_cli_backend_swap_patch_type_checks():
+    """integration/cacesim_main_gpu.patch (the simulate / compare / ablate
+    backend swap, cacesim_main.cpp:194,330) applies to the reference CLI and
+    type-checks against cacesim_gpu.hpp (needs /root/reference: skipped
+    elsewhere)."""
+    import os
+    import subprocess
+
+    if not os.path.isdir("/root/reference/proj/tools"):
+        pytest.skip("reference sources not present")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["make", "-s", "-C", os.path.join(root, "integration"), "cli-check"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -387,4 +387,3 @@ def test_reference_side_binding_drop_in():
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ADAPTER ALL_OK" in out.stdout
-
