@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--capacity", type=int, default=3, help="cfg2/cfg3 capacity (memory budget fits 3)")
     ap.add_argument("--requests", type=int, default=None, help="requests per trace (cfg4 100k, cfg5 10M)")
     ap.add_argument("--seeds", type=int, default=32)
+    ap.add_argument("--capacities", default="1,2,3,4,5,6,7,8", help="cfg4 capacities (experiments; default 1..8)")
     ap.add_argument("--scenarios", type=int, default=8192, help="cfg5 scenario count")
     ap.add_argument("--vectors-stride", type=int, default=1, help="subsample the 4096 weight vectors (debug)")
     ap.add_argument("--parity-sample", type=int, default=1024,
@@ -85,13 +86,15 @@ def workload(args, part: int = 0):
     catalog = synth.eight_model_catalog()
     traces = [synth.mixed_trace(catalog, args.requests, seed=1 + part * args.seeds + s) for s in range(args.seeds)]
     pols = synth.weight_vectors_cfg3()[:: args.vectors_stride]
-    sc = synth.scenario_grid(pols, range(1, 9), args.seeds, catalog.max_expected_output_tokens())
+    caps = [int(c) for c in args.capacities.split(",")]
+    sc = synth.scenario_grid(pols, caps, args.seeds, catalog.max_expected_output_tokens())
     return catalog, traces, sc
 
 
 def workload_name(args, S, n):
     if args.config == 4:
-        return "BASELINE config 4: 4096 weight vectors x capacities 1..8 x %d seeds x %d requests" % (args.seeds, n)
+        caps = "1..8" if args.capacities == "1,2,3,4,5,6,7,8" else "{" + args.capacities + "}"
+        return "BASELINE config 4: 4096 weight vectors x capacities %s x %d seeds x %d requests" % (caps, args.seeds, n)
     if args.config == 3:
         return "BASELINE config 3: 4096 weight vectors x one %d-request trace, capacity %d" % (n, args.capacity)
     if args.config == 2:

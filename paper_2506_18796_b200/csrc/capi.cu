@@ -526,7 +526,10 @@ void dispatch_lane(int dm, int C, const ReplayParams& P, int64_t count, size_t s
   }
 }
 
-constexpr int kWideG = 8;  // lanes per scenario of the wide-pool lane kernel (C / G = 4 slots per lane)
+#ifndef CACE_WIDE_G
+#define CACE_WIDE_G 8
+#endif
+constexpr int kWideG = CACE_WIDE_G;  // lanes per scenario of the wide-pool lane kernel (C / G = 4 slots per lane)
 
 template <int MW, int DM>
 void launch_lane_wide(const ReplayParams& P, int64_t count, cudaStream_t s) {

@@ -239,6 +239,7 @@ struct Window {
   }
   __device__ __forceinline__ void commit(double nxa) {
     const int lane = threadIdx.x & 31;
+    __syncwarp();  // every lane's reads of the table for this request precede the writes
 #pragma unroll
     for (int q = 0; q < MW; ++q) {
       const int m = lane + 32 * q;
@@ -472,8 +473,9 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   // tbound >= |total| of every candidate (p1, p3 in [0, 1]) sets the margin.
   bool screen_ok = true;
   float tbound = 2.0f;
+  const bool writer = !WIDE || lig == 0;  // wide pools: one writer per group's shared columns
   for (int mm = 0; mm < M; ++mm) {
-    S.slot_of[mm * st] = 0;
+    if (writer) S.slot_of[mm * st] = 0;
     // p2 + p4 of model mm (policy.cpp:55, 66-67): exact p4 for the fp64
     // path, fp32 p2 + p4 for screening; ablated terms are 0 exactly as the
     // reference zeroes them
@@ -489,7 +491,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       if (screen_ok) tbound = fmaxf(tbound, 2.0f + (float)b);
     }
   }
-  if (WIDE) {
+  if (WIDE && writer) {
     // fp32 p2 + p4 = fma(p4s, tokens, p2s * p2): the roundings of p2, w1 /
     // normalizer and the fma add <= 2^-22 (|p2| + |p4|) to the screen's
     // error, covered by the doubled coefficient of the margin below
@@ -499,11 +501,16 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   // screen constants live in shared memory: read only by deciding lanes, so
   // they hold no registers across the replay loop
   // (fp32 p1 = p1s * p1v + p1o: verbatim p1v, prose 1 - p1v, ablated 0)
-  S.ud[0] = sc.unload_time_s;  // read on evictions only
-  S.prm[0] = 1.0f / (float)sc.window_length;
-  S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
-  S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
-  S.prm[3 * st] = screen_ok ? 6e-5f + (WIDE ? 2e-6f : 1e-6f) * (tbound + 4.0f) : INFINITY;
+  if (writer) {
+    S.ud[0] = sc.unload_time_s;  // read on evictions only
+    S.prm[0] = 1.0f / (float)sc.window_length;
+    S.prm[st] = variant == CACE_MINUS_P1 ? 0.0f : (verbatim ? 1.0f : -1.0f);
+    S.prm[2 * st] = variant == CACE_MINUS_P1 || verbatim ? 0.0f : 1.0f;
+    S.prm[3 * st] = screen_ok ? 6e-5f + (WIDE ? 2e-6f : 1e-6f) * (tbound + 4.0f) : INFINITY;
+  }
+#ifndef CACE_HOST_EMULATION
+  if (WIDE) __syncwarp();  // the leaders' column set-up precedes every lane's reads
+#endif
 
   int dslot = -1;
   int64_t doff = 0, dn_ev = 0;
@@ -585,6 +592,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       double ud = 0.0;
       if (occ < cap) {  // free slot, no unload delay (engine.cpp:184-187)
         v = occ++;
+        if (WIDE) __syncwarp(gmask);  // the group's reads of slot_of precede the leader's writes
       } else {
         CACE_STAT(1, k);
         if constexpr (!WIDE) {
@@ -910,7 +918,8 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         }
         // residents.erase(victim); evictions++ (engine.cpp:205-206)
         const int vm = slot_model(S.slot[v * st].word);
-        S.slot_of[vm * st] = 0;
+        if (WIDE) __syncwarp(gmask);  // the group's reads of the slots precede the leader's writes
+        if (writer) S.slot_of[vm * st] = 0;
         he = hmix(he, dbits(ct) ^ ((uint64_t)vm << 32));
         if (DM == 1 && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
@@ -927,8 +936,10 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       const double r = (ct + ud) + lt;
       lw = r - ct;
       lo_sum += lt;
-      S.slot[v * st].word = m | (K.lex[m] << 18);
-      S.slot_of[m * st] = (uint8_t)(v + 1);
+      if (writer) {
+        S.slot[v * st].word = m | (K.lex[m] << 18);
+        S.slot_of[m * st] = (uint8_t)(v + 1);
+      }
       ct = r;
       cw = 0u;
       hs = v;
@@ -941,11 +952,13 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     const double ttft = qd + pf;
     const double e2e = ttft + dc;
     const double done = (now + pf) + dc;
-    {
+    if (WIDE) __syncwarp(gmask);  // the group's reads of slot hs precede the write
+    if (writer) {
       SlotEnt* const sp = &S.slot[hs * st];  // one address for both stores
       sp->done = done;
       sp->seq = k;
     }
+    if (WIDE) __syncwarp(gmask);  // visible to the group's reads of the next request
     if ((mc >> 16) == CACE_COMPLETION) {
       sttft += ttft;
       mttft = ttft > mttft ? ttft : mttft;

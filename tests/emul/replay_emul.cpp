@@ -34,6 +34,7 @@ static inline unsigned __float_as_uint(float f) { unsigned u; std::memcpy(&u, &f
 static inline float __fdividef(float a, float b) { return a / b; }
 static inline int __ffs(unsigned x) { return __builtin_ffs((int)x); }
 template <typename T> static inline T __shfl_xor_sync(unsigned, T x, int) { return x; }  // groups of one lane
+static inline void __syncwarp(unsigned = 0xffffffffu) {}
 
 #include "../../paper_2506_18796_b200/csrc/replay_lane.cuh"
 #include "../../paper_2506_18796_b200/csrc/layout.hpp"
