@@ -513,10 +513,14 @@ void dispatch_warp(bool dump, int spl, const ReplayParams& P, int64_t count, cud
 }
 
 void dispatch_lane(int dm, int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s,
-                   bool latency) {
+                   int minb) {
   const bool mw1 = P.cat.M <= 32;
-  if (latency && dm == 0 && mw1) {
+  if (dm == 0 && mw1 && minb == kLaneLatencyMinBlocks) {
     dispatch_lane_c<1, 0, kLaneLatencyMinBlocks>(C, P, count, smem, s);
+    return;
+  }
+  if (dm == 0 && mw1 && minb == kLaneMidMinBlocks) {
+    dispatch_lane_c<1, 0, kLaneMidMinBlocks>(C, P, count, smem, s);
     return;
   }
   switch (dm) {
@@ -588,7 +592,7 @@ ReplayParams replay_params(const cace_engine* e, const cace_scenario_t* d_sc, ca
 
 // One launch over plan entries [b, e) of segment g (b warp-aligned).
 void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams P, int64_t b,
-                  int64_t end, cudaStream_t ws, bool latency) {
+                  int64_t end, cudaStream_t ws, int minb) {
   P.seg_begin = b;
   P.seg_end = end;
   const bool dump_on = P.dump.slot != nullptr;
@@ -599,7 +603,7 @@ void launch_piece(const cace_engine* e, const cace_engine::Seg& g, ReplayParams 
   else if (g.wide)
     dispatch_lane_wide(dm, P, end - b, ws);
   else
-    dispatch_lane(dm, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, latency);
+    dispatch_lane(dm, g.C, P, end - b, lane_smem_bytes(e->cat.M, g.C, dump_on), ws, minb);
 }
 
 void fill_status(cace_engine* e, cace_summary_t* d_out, cudaStream_t s) {
@@ -633,24 +637,24 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   // worker streams so they share the SMs (one segment alone is often less
   // than a wave), then join back onto s.
   const size_t nseg = e->segs.size();
-  // Shallow sweeps (< 5 waves of lane warps) are bound by each warp's
-  // per-request dependency chain: use the register-rich instantiations.
+  // Occupancy tier by sweep depth in waves of 20-warp-per-SM lane warps:
+  // < 1.5 waves the step is one warp's dependency chain (register-rich
+  // MINB 3), 1.5-4.5 waves MINB 4, deeper sweeps are issue-bound (MINB 5).
+  // Measured on config-4 shards (131k / 262k / 524k / 1M scenarios).
   int64_t lane_warps = 0;
   for (const auto& g : e->segs)
     if (!g.warp) lane_warps += (g.e - g.b) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
-  static const int waves = [] {
-    const char* v = std::getenv("CACE_LATENCY_WAVES");  // tuning override
-    return v ? std::atoi(v) : 5;
-  }();
-  const bool latency = lane_warps < (int64_t)waves * sms * (CACE_LANE_MIN_BLOCKS * LANE_BLOCK / 32);
+  const double waves = (double)lane_warps / ((double)sms * (CACE_LANE_MIN_BLOCKS * LANE_BLOCK / 32));
+  int minb = waves < 1.5 ? kLaneLatencyMinBlocks : (waves < 4.5 ? kLaneMidMinBlocks : CACE_LANE_MIN_BLOCKS);
+  if (const char* v = std::getenv("CACE_LANE_MINB")) minb = std::atoi(v);  // tuning override (3, 4, 5)
   if (nseg > 0) {
     if (nseg > 1) fork_workers(e, s, nseg);
     for (size_t k = 0; k < nseg; ++k) {
       cudaStream_t ws = nseg == 1 ? s : e->workers[k % e->workers.size()];
       const auto& g = e->segs[k];
-      launch_piece(e, g, P, g.b, g.e, ws, latency);
+      launch_piece(e, g, P, g.b, g.e, ws, minb);
       ++e->last_launches;
     }
     if (nseg > 1) join_workers(e, s, nseg);
@@ -1060,7 +1064,7 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
       ReplayParams P = P0;
       P.dump.dump_off = d_off.p + c.base;
       P.dump.samples = ring[r].p;
-      launch_piece(e, e->segs[c.seg], P, c.b, c.e, ws, false);
+      launch_piece(e, e->segs[c.seg], P, c.b, c.e, ws, CACE_LANE_MIN_BLOCKS);
       ++e->last_launches;
       CK(cudaEventRecord(ss.rep[r], ws));
       if (pt.on) CK(cudaEventRecord(tl[3 * j + 1], ws));
