@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default="auto", choices=["auto", "lane", "warp"],
                     help="engine kernel mapping (auto = the planner's choice)")
+    ap.add_argument("--metrics", action="store_true",
+                    help="time the on-device RunMetrics pipeline (run_metrics: replay + nearest-rank p50/p95/p99/max "
+                         "per scenario and class) end to end instead of the summary replay (N = 1)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="strong: one sweep split over the ranks (default); weak: every rank its own full sweep")
     return ap.parse_args()
@@ -243,12 +246,63 @@ def run_reference_arm(args):
     }))
 
 
+def run_metrics_mode(args):
+    """compute_run_metrics (metrics.cpp:35-62) of every scenario of the sweep
+    through the public API (`run_metrics`, host buffers in and out), timed
+    wall-clock per call after warm-up; a stratified sample is checked against
+    the reference's compute_run_metrics(run(...)) (oracle/_ref)."""
+    import paper_2506_18796_b200 as P
+
+    catalog, traces, sc = workload(args)
+    n_req = args.requests
+    for _ in range(args.warmup):
+        P.run_metrics(traces, catalog, sc)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        got = P.run_metrics(traces, catalog, sc)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    parity = None
+    if args.parity_sample > 0 and len(catalog) <= 16:
+        from oracle import ref
+        from tests.helpers import ref_catalog, ref_scenario, ref_trace
+
+        rcat = ref_catalog(ref, catalog)
+        idx = stratified_sample(sc, args.parity_sample, 4242)
+        ok = True
+        for i in idx:
+            want = ref.run_metrics(rcat, ref_trace(traces[int(sc[i]["trace"])]), ref_scenario(ref, sc[i]))
+            g = got[i]
+            ok &= all(np.float64(g[f]).view(np.uint64) == np.float64(want[f]).view(np.uint64)
+                      for f in ("cache_hit_rate", "load_overhead_s", "evictions"))
+            for lf in ("ttft_completion", "e2e_reasoning"):
+                ok &= int(g[lf]["count"]) == want[lf]["count"]
+                ok &= all(np.float64(g[lf][q]).view(np.uint64) == np.float64(want[lf][q]).view(np.uint64)
+                          for q in ("p50_s", "p95_s", "p99_s", "max_s"))
+                ok &= abs(float(g[lf]["mean_s"]) - want[lf]["mean_s"]) <= 1e-12 * abs(want[lf]["mean_s"])
+        parity = {"scenarios": int(len(idx)), "percentiles_bit_exact_mean_1e-12": bool(ok),
+                  "sample": "stratified over (capacity, variant, P1 mode, window), reference compute_run_metrics"}
+    print(json.dumps({
+        "metric": "scenario-requests replayed/sec with per-scenario RunMetrics (p50/p95/p99/max TTFT and E2E)",
+        "value": len(sc) * n_req / t, "unit": "scenario-requests/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, len(sc), n_req), "scenarios": len(sc), "requests_per_trace": n_req,
+                   "path": "paper_2506_18796_b200.run_metrics -> cace_run_metrics_batch (C ABI), host buffers, "
+                           "wall clock per call"},
+        "parity_sample": parity, "host": host_info()}))
+
+
 def main():
     args = parse()
     if args.requests is None:
         args.requests = {2: 10_000, 5: 10_000_000}.get(args.config, 100_000)
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.metrics:
+        run_metrics_mode(args)
         return
     import torch
 

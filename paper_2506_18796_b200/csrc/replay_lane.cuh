@@ -105,26 +105,6 @@ __device__ __forceinline__ bool sc_le(double d, uint32_t q, const Cursor& c) {
 }
 
 constexpr unsigned kFull = 0xffffffffu;
-
-// model -> slot map access.  CACE_SOF_ASM: through a 32-bit shared::cta
-// address computed once per scenario and ld/st.shared in PTX (the map is only
-// ever touched through these, so volatile ordering among them suffices);
-// default: the lane's generic pointer.
-#if defined(CACE_SOF_ASM) && !defined(CACE_HOST_EMULATION)
-__device__ __forceinline__ int sof_ld(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
-  return (int)v;
-}
-__device__ __forceinline__ void sof_st(uint32_t a, int v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
-}
-#define CACE_SOF_LD(i) sof_ld(sof_a + (uint32_t)(i) * (uint32_t)st)
-#define CACE_SOF_ST(i, v) sof_st(sof_a + (uint32_t)(i) * (uint32_t)st, (v))
-#else
-#define CACE_SOF_LD(i) ((int)S.slot_of[(i) * st])
-#define CACE_SOF_ST(i, v) (S.slot_of[(i) * st] = (uint8_t)(v))
-#endif
 constexpr float kLn2f = 0.693147180559945309f;
 
 #ifdef CACE_HOST_EMULATION
@@ -488,9 +468,6 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const double norm = (double)sc.output_token_normalizer;
 
   const int st = S.stride;
-#if defined(CACE_SOF_ASM) && !defined(CACE_HOST_EMULATION)
-  const uint32_t sof_a = (uint32_t)__cvta_generic_to_shared(S.slot_of);
-#endif
   // fp32 screening is valid while every p2 + p4 is finite and moderate; the
   // event clock is finite (validated on the host) and t < 1e30 below.
   // tbound >= |total| of every candidate (p1, p3 in [0, 1]) sets the margin.
@@ -498,7 +475,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   float tbound = 2.0f;
   const bool writer = !WIDE || lig == 0;  // wide pools: one writer per group's shared columns
   for (int mm = 0; mm < M; ++mm) {
-    if (writer) CACE_SOF_ST(mm, 0);
+    if (writer) S.slot_of[mm * st] = 0;
     // p2 + p4 of model mm (policy.cpp:55, 66-67): exact p4 for the fp64
     // path, fp32 p2 + p4 for screening; ablated terms are 0 exactly as the
     // reference zeroes them
@@ -595,7 +572,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
     }
 
     // classify (engine.cpp:163-173): resident (never Loading here) -> hit
-    int hs = CACE_SOF_LD(m) - 1;
+    int hs = (int)S.slot_of[m * st] - 1;
     double lw = 0.0;
     const bool hit = hs >= 0;
     if (hit) {
@@ -942,7 +919,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         // residents.erase(victim); evictions++ (engine.cpp:205-206)
         const int vm = slot_model(S.slot[v * st].word);
         if (WIDE) __syncwarp(gmask);  // the group's reads of the slots precede the leader's writes
-        if (writer) CACE_SOF_ST(vm, 0);
+        if (writer) S.slot_of[vm * st] = 0;
         he = hmix(he, dbits(ct) ^ ((uint64_t)vm << 32));
         if (DM == 1 && dslot >= 0) {
           if (dn_ev < P.dump.evict_cap) {
@@ -961,7 +938,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       lo_sum += lt;
       if (writer) {
         S.slot[v * st].word = m | (K.lex[m] << 18);
-        CACE_SOF_ST(m, v + 1);
+        S.slot_of[m * st] = (uint8_t)(v + 1);
       }
       ct = r;
       cw = 0u;

@@ -1,4 +1,4 @@
-# round-2: occupancy tiers by sweep depth (MINB 3 / 4 / 5) on the in-tree library.
-OUT=gpurun_out; mkdir -p $OUT; TAG=r2n
-timeout 1500 python -m pytest tests -m gpu -x -q -rf --timeout 900 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_$TAG.log
-AB_ARGS="--seeds 32;--seeds 16;--seeds 8;--seeds 4;--config 3" bash tools/gpu_ab_env.sh ${TAG}_tiers "" "CACE_LANE_MINB=5"
+# round-2: RunMetrics line (config 4 and config 3) through the public API.
+OUT=gpurun_out; mkdir -p $OUT; TAG=r2p
+timeout 1200 python bench.py --metrics --steps 2 --warmup 1 --parity-sample 32 > $OUT/bench_metrics_cfg4_$TAG.log 2>&1
+timeout 600 python bench.py --metrics --config 3 --steps 3 --warmup 1 --parity-sample 32 > $OUT/bench_metrics_cfg3_$TAG.log 2>&1
