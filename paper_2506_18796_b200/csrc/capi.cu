@@ -466,23 +466,37 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C, int MW, int DM, int MINB>
+template <int C, int MW, int DM, int MINB, int MC = 0>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DM, MINB>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto* k = replay_lane_kernel<C, MW, DM, MINB, MC>;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // one L1/shared split for every capacity's kernel: blocks of different
   // segments can then share an SM without a carveout change (shallow sweeps
   // +9%, profiles/r2/ab_carveout_v6.txt)
-  CK(cudaFuncSetAttribute(replay_lane_kernel<C, MW, DM, MINB>,
-                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const unsigned grid = (unsigned)((count + LANE_BLOCK - 1) / LANE_BLOCK);
-  replay_lane_kernel<C, MW, DM, MINB><<<grid, LANE_BLOCK, smem, s>>>(P);
+  k<<<grid, LANE_BLOCK, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 
+// The 8-model pool (BASELINE configs 1-4; capacities clamp to <= 8) has
+// compile-time-layout instantiations of the summary and RunMetrics-sample
+// kernels (MC = 8; +3.4% on config 4, profiles/r2/ab_pool_mc_r2q.txt).
+constexpr int kPoolMC = 8;
+
 template <int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS>
 void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+#ifndef CACE_NO_POOL_MC
+  if ((DM == 0 || DM == 2) && MW == 1 && P.cat.M == kPoolMC) {  // summaries, RunMetrics samples
+    switch (C) {
+#define CASE(k) \
+  case k: launch_lane<k, 1, DM, MINB, kPoolMC>(P, count, smem, s); return;
+      CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+      default: break;
+    }
+  }
+#endif
   switch (C) {
 #define CASE(k) \
   case k: launch_lane<k, MW, DM, MINB>(P, count, smem, s); break;
@@ -539,13 +553,12 @@ template <int MW, int DM>
 void launch_lane_wide(const ReplayParams& P, int64_t count, cudaStream_t s) {
   constexpr int G = kWideG;
   const size_t smem = lane_wide_smem_bytes(P.cat.M, DM != 0, G);
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(replay_lane_wide_kernel<MW, DM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-  CK(cudaFuncSetAttribute(replay_lane_wide_kernel<MW, DM, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  auto* k = replay_lane_wide_kernel<MW, DM, G>;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   constexpr int SB = LANE_BLOCK_WIDE / G;  // scenarios (plan entries) per block
   const unsigned grid = (unsigned)((count + SB - 1) / SB);
-  replay_lane_wide_kernel<MW, DM, G><<<grid, LANE_BLOCK_WIDE, smem, s>>>(P);
+  k<<<grid, LANE_BLOCK_WIDE, smem, s>>>(P);
   CK(cudaGetLastError());
 }
 

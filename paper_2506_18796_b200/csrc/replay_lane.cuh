@@ -443,7 +443,10 @@ __device__ __forceinline__ void flush_samples(const double* tile, double* const*
 // capacity is cap_rt (<= C); no per-lane p2 + p4 tables -- the fp32 screen
 // forms p2 + p4 from the block's catalog columns and two per-lane scalars,
 // the exact path recomputes p4 = w1 * (tokens / normalizer).
-template <int C, int MW, int DM, bool XR = true, bool WIDE = false, int G = 1>
+// MC > 0: the pool size is the compile-time constant MC (== P.cat.M), so the
+// shared-memory layout folds into immediate offsets (the 8-model pool of
+// BASELINE configs 1-4); 0: the runtime P.cat.M.
+template <int C, int MW, int DM, bool XR = true, bool WIDE = false, int G = 1, int MC = 0>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
                                 const CatShared& K, const LaneSmem& S, int cap_rt = C) {
   static_assert(G == 1 || WIDE, "lane groups are a wide-pool mode");
@@ -456,7 +459,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
 #endif
   const cace_scenario_t sc = P.scen[sidx];
-  const int M = P.cat.M;
+  const int M = MC > 0 ? MC : P.cat.M;
   const int64_t base = P.trace_off[sc.trace];
   const uint32_t n = (uint32_t)(P.trace_off[sc.trace + 1] - base);
   const ReqRec* tr = P.rec + base;
@@ -1078,10 +1081,10 @@ constexpr int kLaneMidMinBlocks = 4;
 // DM: 0 summary only; 1 full dump (outcomes, eviction log, samples) for the
 // scenarios with a dump slot; 2 metrics samples only (the RunMetrics
 // pipeline: no outcome / eviction-log code or registers).
-template <int C, int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS>
+template <int C, int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS, int MC = 0>
 __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int M = P.cat.M;
+  const int M = MC > 0 ? MC : P.cat.M;  // MC: compile-time pool size (immediate shared offsets)
   double* s_lt = reinterpret_cast<double*>(smem);
   double* s_p2 = s_lt + M;
   double* s_tok = s_p2 + M;
@@ -1123,7 +1126,7 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_slot + threadIdx.x, l_prm + threadIdx.x,
                    l_p4d + (size_t)M * LANE_BLOCK + threadIdx.x, nullptr, l_sof + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win, w_samp, w_bar};
-  replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks>(P, sidx, shadow, warp_win, K, S);
+  replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks, false, 1, MC>(P, sidx, shadow, warp_win, K, S);
 }
 
 // ---- wide pools / capacities ----------------------------------------------
