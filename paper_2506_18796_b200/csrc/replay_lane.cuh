@@ -190,7 +190,10 @@ struct Window {
     fa[mk] = nxa;
   }
 #else
-  uint32_t f[MW], r[MW];
+  // ranks are kept as floats (exact small integers; the table stores them as
+  // floats) so committing them needs no conversion
+  uint32_t f[MW];
+  float r[MW];
   int M;
   WinEnt* tab;
   __device__ __forceinline__ void init(const uint32_t* f0, int M_, const ReqRec* tr, uint32_t n,
@@ -204,7 +207,7 @@ struct Window {
       f[q] = m < M ? __ldg(f0 + m) : 0xffffffffu;
       uint32_t c = 0;
       for (int mm = 0; mm < M; ++mm) c += __ldg(f0 + mm) < f[q] ? 1u : 0u;
-      r[q] = c;
+      r[q] = (float)c;
       if (m < M) tab[m] = WinEnt{f[q], (float)c, f[q] < n ? __ldg(&tr[f[q]].arrival) : INFINITY};
     }
     __syncwarp();
@@ -215,21 +218,25 @@ struct Window {
   // served -- mk's first becomes nx -- without touching what the iteration's
   // decisions read; commit installs it.  (Issuing prepare at the top of the
   // iteration to overlap the ballot latency measured slower; the replay loop
-  // calls them back to back at the end.)
-  uint32_t nf[MW], nr[MW];
+  // calls them back to back at the end.)  mk's new rank = the number of other
+  // models whose first pending request precedes nx: each lane counts its own
+  // models, one warp reduction sums them.
+  uint32_t nf[MW];
+  float nr[MW];
   int pmk;
   __device__ __forceinline__ void prepare(int mk, uint32_t nx) {
     const int lane = threadIdx.x & 31;
     pmk = mk;
-    uint32_t cnt = 0;
+    uint32_t lc = 0;
 #pragma unroll
     for (int q = 0; q < MW; ++q) {
       const int m = lane + 32 * q;
       const bool before = m < M && m != mk && f[q] < nx;
-      cnt += __popc(__ballot_sync(kFull, before));
+      lc += before ? 1u : 0u;
       nf[q] = f[q];
-      nr[q] = before ? r[q] - 1 : r[q];
+      nr[q] = before ? r[q] - 1.0f : r[q];
     }
+    const float cnt = (float)__reduce_add_sync(kFull, lc);
 #pragma unroll
     for (int q = 0; q < MW; ++q)
       if (lane + 32 * q == mk) {
@@ -246,7 +253,7 @@ struct Window {
       f[q] = nf[q];
       r[q] = nr[q];
       if (m == pmk) tab[m].fa = nxa;
-      if (m < M) *reinterpret_cast<uint2*>(&tab[m]) = make_uint2(f[q], __float_as_uint((float)r[q]));
+      if (m < M) *reinterpret_cast<uint2*>(&tab[m]) = make_uint2(f[q], __float_as_uint(r[q]));
     }
     __syncwarp();
   }
@@ -1075,7 +1082,10 @@ inline size_t lane_smem_bytes(int M, int C, bool dump) {
 // warps/SM, 114 registers, no spills) for 1.5-4.5 waves; 3 (12 warps/SM, up
 // to 168 registers, the exact fallback unrolled: the shortest per-request
 // dependency chain) below 1.5 waves, where each warp's chain bounds the step.
-constexpr int kLaneLatencyMinBlocks = 3;
+#ifndef CACE_LANE_LAT_MINB
+#define CACE_LANE_LAT_MINB 3
+#endif
+constexpr int kLaneLatencyMinBlocks = CACE_LANE_LAT_MINB;
 constexpr int kLaneMidMinBlocks = 4;
 
 // DM: 0 summary only; 1 full dump (outcomes, eviction log, samples) for the
