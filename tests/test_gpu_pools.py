@@ -45,3 +45,38 @@ def test_large_pool_full_report_vs_port():
         want = port.run(port.Catalog(catalog), t, row)
         assert np.array_equal(bits(rep.ttft_s), bits(want.ttft)) and np.array_equal(bits(rep.e2e_s), bits(want.e2e))
         assert np.array_equal(rep.evicted_model, want.evict_model)
+
+
+def test_capacity_beyond_the_pool_is_accepted(ref):
+    """The reference accepts any num_accelerators x models_per_accelerator
+    (engine.cpp:83-84); with capacity >= the pool nothing is ever evicted, so
+    the engine clamps it to the pool size: capacities up to 3000 replay
+    bit-exact against the reference (16 models) and the port (48 models,
+    clamped to 48 slots: the warp kernel).  Pools of more than 64 models with a
+    capacity above 64 are rejected (CACE_E_INVALID)."""
+    import paper_2506_18796_b200 as P
+    from oracle import port
+    from paper_2506_18796_b200 import api, synth
+    from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig
+    from tests.helpers import ref_catalog, ref_scenario, ref_trace
+
+    cat16 = api.ModelCatalog.build_default()
+    traces = [synth.mixed_trace(cat16, 3000, seed=41)]
+    rows = [(0, PolicyConfig(variant=v, window_length=8), ClusterConfig(num_accelerators=a, models_per_accelerator=mpa))
+            for v in (0, 1) for a, mpa in ((16, 1), (17, 1), (65, 1), (100, 3), (1000, 3))]
+    sc = api.make_scenarios(rows)
+    got = P.run_batch(traces, cat16, sc)
+    assert (got["evictions"] == 0).all()
+    want, _ = ref.run_batch(ref_catalog(ref, cat16), [ref_trace(t) for t in traces], [ref_scenario(ref, r) for r in sc])
+    assert_summaries_equal(got, want, "capacity >= pool (16 models)")
+    cat48 = api.ModelCatalog.synthetic_pool(48, seed=8)
+    t48 = [synth.mixed_trace(cat48, 3000, seed=42, rate=5.0)]
+    rows = [(0, PolicyConfig(variant=1, window_length=64), ClusterConfig(num_accelerators=a)) for a in (48, 49, 200, 3000)]
+    sc = api.make_scenarios(rows)
+    got = P.run_batch(t48, cat48, sc)
+    want, _ = port.run_batch(port.Catalog(cat48), t48, sc)
+    assert_summaries_equal(got, want, "capacity >= pool (48 models)")
+    cat80 = api.ModelCatalog.synthetic_pool(80, seed=8)
+    t80 = [synth.mixed_trace(cat80, 500, seed=43)]
+    with pytest.raises(P.SimError):
+        P.run_batch(t80, cat80, api.make_scenarios([(0, PolicyConfig(), ClusterConfig(num_accelerators=80))]))
