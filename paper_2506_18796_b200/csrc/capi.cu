@@ -9,10 +9,12 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <numeric>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/cace_gpu.h"
@@ -273,46 +275,99 @@ struct cace_engine {
   std::vector<cudaStream_t> workers;  // fork/join streams for capacity segments
   std::vector<cudaEvent_t> joins;
   cudaEvent_t fork = nullptr;
+  bool pooled = false;          // streams/events borrowed from the process-wide pool
+  cudaStream_t pool_stream = nullptr;
+  bool upload_pending = false;  // trace upload in flight from the pinned arena (finish_upload)
+  bool arena_held = false;
 };
 
 namespace {
 
 constexpr int kWorkers = 8;
 
+// Process-wide pool of engine stream sets (own stream + workers + fork/join
+// events) per device: creating and destroying 9 streams and 9 events per
+// cace_replay_batch call costs milliseconds of host time; engines borrow a
+// set exclusively and return it idle (synchronised) on destroy.
+struct StreamSet {
+  cudaStream_t stream;
+  std::vector<cudaStream_t> workers;
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork;
+};
+struct StreamPool {
+  std::mutex mu;
+  std::vector<std::pair<int, StreamSet>> free_sets;  // (device, set)
+  bool take(int dev, StreamSet& out) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < free_sets.size(); ++i)
+      if (free_sets[i].first == dev) {
+        out = free_sets[i].second;
+        free_sets.erase(free_sets.begin() + (long)i);
+        return true;
+      }
+    return false;
+  }
+  void give(int dev, const StreamSet& st) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_sets.push_back({dev, st});
+  }
+} g_streams;
+
+// The trace records travel from the pinned arena asynchronously while the
+// host plans; the first synchronisation of the engine stream completes them.
+void finish_upload(cace_engine* e) {
+  if (!e->upload_pending) return;
+  CK(cudaStreamSynchronize(e->stream));
+  e->upload_pending = false;
+  decltype(e->lay.rec)().swap(e->lay.rec);  // device copy is authoritative
+  e->lay.ext_rec = nullptr;
+  std::vector<uint32_t>().swap(e->lay.perm);
+  if (e->arena_held) {
+    g_arena.release();
+    e->arena_held = false;
+  }
+}
+
 void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trace_t* traces,
-                  int32_t n_traces, const cace_opts_t* opts) {
+                  int32_t n_traces, const cace_opts_t* opts, bool defer_sync = false) {
   require_device(opts);
   e->device = opts ? opts->device : 0;
+  StreamSet ss;
+  if (g_streams.take(e->device, ss)) {
+    e->pooled = true;
+  } else {
+    CK(cudaStreamCreateWithFlags(&ss.stream, cudaStreamNonBlocking));
+    for (int k = 0; k < kWorkers; ++k) {
+      cudaStream_t ws;
+      cudaEvent_t ev;
+      CK(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ss.workers.push_back(ws);
+      ss.joins.push_back(ev);
+    }
+    CK(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    e->pooled = true;
+  }
+  e->workers = ss.workers;
+  e->joins = ss.joins;
+  e->fork = ss.fork;
   if (opts && opts->stream) {
     e->stream = static_cast<cudaStream_t>(opts->stream);
   } else {
-    CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->stream = ss.stream;
     e->own_stream = true;
   }
+  e->pool_stream = ss.stream;
   e->log_variant = resolve_log_variant(opts);
   e->kernel_pref = opts ? opts->kernel : CACE_KERNEL_AUTO;
-  for (int k = 0; k < kWorkers; ++k) {
-    cudaStream_t ws;
-    cudaEvent_t ev;
-    CK(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    e->workers.push_back(ws);
-    e->joins.push_back(ev);
-  }
-  CK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
   PhaseTimer pt;
   e->cat.load(catalog);
-  struct ArenaGuard {
-    bool held = false;
-    ~ArenaGuard() {
-      if (held) g_arena.release();
-    }
-  } guard;
   if (n_traces > 0 && traces) {
     const int64_t N = layout_requests(traces, n_traces);
     if (N >= (1 << 16)) {
       e->lay.ext_rec = static_cast<ReqRec*>(g_arena.acquire((size_t)N * sizeof(ReqRec)));
-      guard.held = e->lay.ext_rec != nullptr;
+      e->arena_held = e->lay.ext_rec != nullptr;
     }
   }
   build_layout(e->cat, traces, n_traces, e->lay);
@@ -326,11 +381,11 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
   e->d_ncomp.upload(e->lay.ncomp.data(), e->lay.ncomp.size(), s);
   e->d_tab.upload(kLogTab, 256, s);
   e->d_tab2.upload(kLogTab2, 256, s);
-  CK(cudaStreamSynchronize(s));
-  pt.mark("  upload");
-  decltype(e->lay.rec)().swap(e->lay.rec);  // device copy is authoritative
-  e->lay.ext_rec = nullptr;
-  std::vector<uint32_t>().swap(e->lay.perm);
+  e->upload_pending = true;
+  if (!defer_sync) {
+    finish_upload(e);
+    pt.mark("  upload");
+  }
 }
 
 void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
@@ -462,6 +517,7 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
   e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);
   CK(cudaStreamSynchronize(e->stream));
+  finish_upload(e);
   e->h_order = std::move(order);
   e->plan_n = n;
 }
@@ -691,6 +747,26 @@ int32_t guarded(char* msg, size_t cap, F&& f) {
   }
 }
 
+// cace_engine_create, optionally leaving the trace upload in flight (the
+// first plan() completes it; cace_replay_batch overlaps the two).
+int32_t engine_create_impl(const cace_catalog_t* catalog, const cace_trace_t* traces, int32_t n_traces,
+                           const cace_opts_t* opts, cace_engine** out, char* msg, size_t msg_cap,
+                           bool defer_sync) {
+  if (!out) return CACE_E_INVALID;
+  *out = nullptr;
+  cace_engine* e = new cace_engine();
+  const int32_t rc = guarded(msg, msg_cap, [&]() -> int32_t {
+    build_engine(e, catalog, traces, n_traces, opts, defer_sync);
+    return CACE_OK;
+  });
+  if (rc != CACE_OK) {
+    cace_engine_destroy(e);
+    return rc;
+  }
+  *out = e;
+  return CACE_OK;
+}
+
 }  // namespace
 
 // ==========================================================================
@@ -705,31 +781,19 @@ int32_t cace_device_count(void) { return device_count(); }
 int32_t cace_engine_create(const cace_catalog_t* catalog, const cace_trace_t* traces,
                            int32_t n_traces, const cace_opts_t* opts, cace_engine** out,
                            char* msg, size_t msg_cap) {
-  if (!out) return CACE_E_INVALID;
-  *out = nullptr;
-  cace_engine* e = new cace_engine();
-  const int32_t rc = guarded(msg, msg_cap, [&]() -> int32_t {
-    build_engine(e, catalog, traces, n_traces, opts);
-    return CACE_OK;
-  });
-  if (rc != CACE_OK) {
-    cace_engine_destroy(e);
-    return rc;
-  }
-  *out = e;
-  return CACE_OK;
+  return engine_create_impl(catalog, traces, n_traces, opts, out, msg, msg_cap, false);
 }
 
 void cace_engine_destroy(cace_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
-  for (auto ws : e->workers) {
-    cudaStreamSynchronize(ws);
-    cudaStreamDestroy(ws);
+  for (auto ws : e->workers) cudaStreamSynchronize(ws);
+  if (e->upload_pending) {  // an engine destroyed before its first plan
+    e->upload_pending = false;
+    e->lay.ext_rec = nullptr;
   }
-  for (auto ev : e->joins) cudaEventDestroy(ev);
-  if (e->fork) cudaEventDestroy(e->fork);
+  if (e->arena_held) g_arena.release();
   // device buffers go back to the pool in order on the engine stream, which
   // must still exist
   e->cat.d_lt.release();
@@ -746,7 +810,17 @@ void cace_engine_destroy(cace_engine* e) {
   e->d_order.release();
   e->d_bad_idx.release();
   e->d_bad_code.release();
-  if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+  if (e->pooled) {
+    // the set goes back idle: its own stream is synchronised after the frees
+    cudaStreamSynchronize(e->pool_stream);
+    if (cudaGetLastError() == cudaSuccess)
+      g_streams.give(e->device, StreamSet{e->pool_stream, e->workers, e->joins, e->fork});
+  } else {
+    for (auto ws : e->workers) cudaStreamDestroy(ws);
+    for (auto ev : e->joins) cudaEventDestroy(ev);
+    if (e->fork) cudaEventDestroy(e->fork);
+    if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+  }
   delete e;
 }
 
@@ -786,16 +860,36 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
                           const cace_opts_t* opts, char* msg, size_t msg_cap) {
   cace_engine* e = nullptr;
   PhaseTimer pt;
-  int32_t rc = cace_engine_create(catalog, traces, n_traces, opts, &e, msg, msg_cap);
+  // the trace records' DMA from the pinned arena overlaps the plan below
+  int32_t rc = engine_create_impl(catalog, traces, n_traces, opts, &e, msg, msg_cap, true);
   if (rc != CACE_OK) return rc;
   pt.mark("engine_create");
   rc = guarded(msg, msg_cap, [&]() -> int32_t {
     if (n_scenarios > 0 && !summaries) throw Invalid{CACE_E_INVALID, "cace: summaries is NULL"};
-    plan(e, scenarios, n_scenarios);
-    pt.mark("plan");
     cudaStream_t s = e->stream;
     DBuf<cace_scenario_t> d_sc;
-    d_sc.upload(scenarios, n_scenarios, s);
+    {
+      // the (pageable) scenario upload runs on a helper thread while this one
+      // plans; both are on the engine stream, ahead of the replay
+      std::exception_ptr up_err;
+      std::thread up([&] {
+        try {
+          CK(cudaSetDevice(e->device));
+          d_sc.upload(scenarios, n_scenarios, s);
+        } catch (...) {
+          up_err = std::current_exception();
+        }
+      });
+      try {
+        plan(e, scenarios, n_scenarios);
+      } catch (...) {
+        up.join();
+        throw;
+      }
+      up.join();
+      if (up_err) std::rethrow_exception(up_err);
+    }
+    pt.mark("plan+upload_scen");
     DBuf<cace_summary_t> d_out;
     d_out.alloc(n_scenarios, s);
     // Optional full dump.
