@@ -262,10 +262,15 @@ struct cace_engine {
     int64_t b, e;
     bool warp;  // warp-per-scenario kernel
     bool wide;  // lane kernel, wide-pool mode (pools > 64 models or capacities > 16)
+    bool mixed = false;  // in the mixed-capacity plan (d_mixed)
   };
   std::vector<Seg> segs;
   std::vector<int64_t> h_order;  // plan entries (scenario index | kShadowBit)
   DBuf<int64_t> d_order;
+  // shallow sweeps: the lane segments of capacity <= kMixedC concatenated
+  // heaviest first, replayed by ONE mixed-capacity launch (d_mixed)
+  int64_t n_mixed = 0;
+  DBuf<int64_t> d_mixed;
   std::vector<int64_t> bad_idx;
   std::vector<int32_t> bad_code;
   DBuf<int64_t> d_bad_idx;
@@ -284,6 +289,7 @@ struct cace_engine {
 namespace {
 
 constexpr int kWorkers = 8;
+constexpr int kMixedC = 8;  // capacity bound of the mixed-capacity (runtime capacity) launch
 
 // Process-wide pool of engine stream sets (own stream + workers + fork/join
 // events) per device: creating and destroying 9 streams and 9 events per
@@ -513,6 +519,20 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   };
   std::stable_sort(e->segs.begin(), e->segs.end(),
                    [&](const cace_engine::Seg& x, const cace_engine::Seg& y) { return seg_cost(x) > seg_cost(y); });
+  // The mixed-capacity plan (shallow sweeps, replay()): every lane segment of
+  // capacity <= kMixedC, heaviest first, as one launch.  Concurrent
+  // per-capacity launches of a few hundred blocks each leave SMs unevenly
+  // loaded (a 2560-warp sweep: 151 ms as five concurrent launches, 92 ms as
+  // one; profiles/r2/ab_concurrency_r2w.txt).
+  {
+    std::vector<int64_t> mixed;
+    for (auto& g : e->segs) {
+      g.mixed = !g.warp && !g.wide && g.C <= kMixedC;
+      if (g.mixed) mixed.insert(mixed.end(), order.begin() + g.b, order.begin() + g.e);
+    }
+    e->n_mixed = (int64_t)mixed.size();
+    e->d_mixed.upload(mixed.data(), mixed.size(), e->stream);
+  }
   e->d_order.upload(order.data(), order.size(), e->stream);
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
   e->d_bad_code.upload(e->bad_code.data(), e->bad_code.size(), e->stream);
@@ -522,9 +542,9 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   e->plan_n = n;
 }
 
-template <int C, int MW, int DM, int MINB, int MC = 0>
+template <int C, int MW, int DM, int MINB, int MC = 0, bool RTC = false>
 void launch_lane(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
-  auto* k = replay_lane_kernel<C, MW, DM, MINB, MC>;
+  auto* k = replay_lane_kernel<C, MW, DM, MINB, MC, RTC>;
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // one L1/shared split for every capacity's kernel: blocks of different
   // segments can then share an SM without a carveout change (shallow sweeps
@@ -561,6 +581,28 @@ void dispatch_lane_c(int C, const ReplayParams& P, int64_t count, size_t smem, c
 #undef CASE
     default: throw Invalid{CACE_E_INVALID, "cace: capacity not supported by the lane kernel"};
   }
+}
+
+// One mixed-capacity launch (RTC instantiation, capacity bound kMixedC) over
+// plan entries [0, count) of P.order.
+template <int MINB>
+void launch_mixed_t(const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+#ifndef CACE_NO_POOL_MC
+  if (P.cat.M == kPoolMC) {
+    launch_lane<kMixedC, 1, 0, MINB, kPoolMC, true>(P, count, smem, s);
+    return;
+  }
+#endif
+  launch_lane<kMixedC, 1, 0, MINB, 0, true>(P, count, smem, s);
+}
+
+void launch_mixed(int minb, const ReplayParams& P, int64_t count, size_t smem, cudaStream_t s) {
+  if (minb == kLaneLatencyMinBlocks)
+    launch_mixed_t<kLaneLatencyMinBlocks>(P, count, smem, s);
+  else if (minb == kLaneMidMinBlocks)
+    launch_mixed_t<kLaneMidMinBlocks>(P, count, smem, s);
+  else
+    launch_mixed_t<CACE_LANE_MIN_BLOCKS>(P, count, smem, s);
 }
 
 template <int SPL, bool DUMP>
@@ -715,18 +757,43 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
     if (!g.warp) lane_warps += (g.e - g.b) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
-  const double waves = (double)lane_warps / ((double)sms * (CACE_LANE_MIN_BLOCKS * LANE_BLOCK / 32));
+  const double waves = (double)lane_warps / ((double)sms * (CACE_LANE_MIN_BLOCKS * 4));
   int minb = waves < 1.5 ? kLaneLatencyMinBlocks : (waves < 4.5 ? kLaneMidMinBlocks : CACE_LANE_MIN_BLOCKS);
   if (const char* v = std::getenv("CACE_LANE_MINB")) minb = std::atoi(v);  // tuning override (3, 4, 5)
-  if (nseg > 0) {
-    if (nseg > 1) fork_workers(e, s, nseg);
-    for (size_t k = 0; k < nseg; ++k) {
-      cudaStream_t ws = nseg == 1 ? s : e->workers[k % e->workers.size()];
-      const auto& g = e->segs[k];
-      launch_piece(e, g, P, g.b, g.e, ws, minb);
+  // From 0.5 to 1.5 waves with several capacities (a strong-scaling shard), the
+  // capacities <= 8 run as ONE mixed-capacity launch at MINB 4 (summaries,
+  // pools <= 32 models): 131k shard 8.6e10 -> 1.21e11; at 262k the
+  // per-capacity launches stay faster, and below 0.5 waves (32k scenarios)
+  // the per-capacity MINB 3 kernels (profiles/r2/ab_mixed_r2y.txt, ab_mixed_r2z.txt).
+  int n_mixable = 0;
+  for (const auto& g : e->segs) n_mixable += g.mixed ? 1 : 0;
+  bool mixed = waves >= 0.5 && waves < 1.5 && dump.slot == nullptr && e->cat.M <= 32 && n_mixable >= 2;
+  if (const char* v = std::getenv("CACE_MIXED")) mixed = v[0] == '1' ? (dump.slot == nullptr && e->cat.M <= 32 &&
+                                                                          n_mixable >= 1)
+                                                                       : false;  // A/B switch (0 / 1)
+  const int minb_mixed = std::getenv("CACE_LANE_MINB") ? minb : kLaneMidMinBlocks;
+  std::vector<const cace_engine::Seg*> launch;
+  for (const auto& g : e->segs)
+    if (!(mixed && g.mixed)) launch.push_back(&g);
+  const size_t nl = launch.size() + (mixed ? 1 : 0);
+  if (nl > 0) {
+    if (nl > 1) fork_workers(e, s, nl);
+    size_t k = 0;
+    if (mixed) {
+      cudaStream_t ws = nl == 1 ? s : e->workers[k++ % e->workers.size()];
+      ReplayParams Q = P;
+      Q.order = e->d_mixed.p;
+      Q.seg_begin = 0;
+      Q.seg_end = e->n_mixed;
+      launch_mixed(minb_mixed, Q, e->n_mixed, lane_smem_bytes(e->cat.M, kMixedC, false), ws);
       ++e->last_launches;
     }
-    if (nseg > 1) join_workers(e, s, nseg);
+    for (const auto* g : launch) {
+      cudaStream_t ws = nl == 1 ? s : e->workers[k++ % e->workers.size()];
+      launch_piece(e, *g, P, g->b, g->e, ws, minb);
+      ++e->last_launches;
+    }
+    if (nl > 1) join_workers(e, s, nl);
   }
   fill_status(e, d_out, s);
 }
@@ -808,6 +875,7 @@ void cace_engine_destroy(cace_engine* e) {
   e->d_tab.release();
   e->d_tab2.release();
   e->d_order.release();
+  e->d_mixed.release();
   e->d_bad_idx.release();
   e->d_bad_code.release();
   if (e->pooled) {

@@ -453,11 +453,14 @@ __device__ __forceinline__ void flush_samples(const double* tile, double* const*
 // MC > 0: the pool size is the compile-time constant MC (== P.cat.M), so the
 // shared-memory layout folds into immediate offsets (the 8-model pool of
 // BASELINE configs 1-4); 0: the runtime P.cat.M.
-template <int C, int MW, int DM, bool XR = true, bool WIDE = false, int G = 1, int MC = 0>
+// RTC: the capacity is cap_rt (<= C, a runtime value) in the one-lane mode
+// too -- one instantiation serves every capacity up to C (the mixed-capacity
+// launch of shallow sweeps).
+template <int C, int MW, int DM, bool XR = true, bool WIDE = false, int G = 1, int MC = 0, bool RTC = false>
 __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow, bool warp_win,
                                 const CatShared& K, const LaneSmem& S, int cap_rt = C) {
   static_assert(G == 1 || WIDE, "lane groups are a wide-pool mode");
-  const int cap = WIDE ? cap_rt : C;
+  const int cap = (WIDE || RTC) ? cap_rt : C;
 #ifdef CACE_HOST_EMULATION
   const int lig = 0;
   const unsigned gmask = 1u;
@@ -614,7 +617,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
         unsigned idm = 0;
 #pragma unroll
         for (int s = 0; s < C; ++s) {
-          if (WIDE && s >= cap) break;
+          if ((WIDE || RTC) && s >= cap) break;
           const SlotEnt e = S.slot[s * st];
           sd[s] = e.done;
           sq[s] = e.seq;
@@ -630,7 +633,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           uint32_t q1 = sq[0];
 #pragma unroll
           for (int s = 1; s < C; ++s) {
-            if (WIDE && s >= cap) break;
+            if ((WIDE || RTC) && s >= cap) break;
             if (sd[s] < t1 || (sd[s] == t1 && sq[s] < q1)) {
               s1 = s;
               t1 = sd[s];
@@ -655,7 +658,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             int flex = 0;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              if (WIDE && s >= cap) break;
+              if ((WIDE || RTC) && s >= cap) break;
               const int lx = slot_lex(sw[s]);
               if ((idm >> s) & 1u)
                 if (f < 0 || sd[s] < flu || (sd[s] == flu && lx < flex)) {
@@ -683,7 +686,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
-              if (WIDE && s >= cap) break;
+              if ((WIDE || RTC) && s >= cap) break;
               const int ms = slot_model(sw[s]);
               const float t = fmaxf((float)(now - sd[s]), 1.0f);  // max(d, 1) in fp32
               const float p1v = fast_rcp(fmaf(fast_lg2(t), kLn2f, 1.0f));
@@ -1051,7 +1054,12 @@ constexpr uint64_t kShadowBit = 1ull << 62;  // plan entry = warp padding lane
 constexpr int kLaneMaxModels = 64;           // lane kernel: window in <= 2 registers/lane
 
 #ifndef CACE_HOST_EMULATION
-constexpr int LANE_BLOCK = 128;
+#ifndef CACE_LANE_BLOCK
+#define CACE_LANE_BLOCK 128
+#endif
+constexpr int LANE_BLOCK = CACE_LANE_BLOCK;  // threads per lane block
+// MINB counts 128-thread blocks per SM (the register target), whatever LANE_BLOCK is
+constexpr int kLaneBlockScale = 128 / LANE_BLOCK;
 #ifndef CACE_LANE_MIN_BLOCKS
 #define CACE_LANE_MIN_BLOCKS 5  // <= 96 registers: 5 blocks (20 warps) per SM
 #endif
@@ -1091,8 +1099,10 @@ constexpr int kLaneMidMinBlocks = 4;
 // DM: 0 summary only; 1 full dump (outcomes, eviction log, samples) for the
 // scenarios with a dump slot; 2 metrics samples only (the RunMetrics
 // pipeline: no outcome / eviction-log code or registers).
-template <int C, int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS, int MC = 0>
-__global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayParams P) {
+// RTC: a mixed-capacity launch -- C is the bound, each warp's capacity is its
+// scenarios' effective capacity (the plan keeps warps capacity-uniform).
+template <int C, int MW, int DM, int MINB = CACE_LANE_MIN_BLOCKS, int MC = 0, bool RTC = false>
+__global__ void __launch_bounds__(LANE_BLOCK, MINB * kLaneBlockScale) replay_lane_kernel(ReplayParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = MC > 0 ? MC : P.cat.M;  // MC: compile-time pool size (immediate shared offsets)
   double* s_lt = reinterpret_cast<double*>(smem);
@@ -1127,16 +1137,19 @@ __global__ void __launch_bounds__(LANE_BLOCK, MINB) replay_lane_kernel(ReplayPar
   const uint64_t e = (uint64_t)P.order[gi];
   const bool shadow = (e & kShadowBit) != 0;
   const int64_t sidx = (int64_t)(e & (kShadowBit - 1));
-  const int variant = P.scen[sidx].variant;
+  const cace_scenario_t& scn = P.scen[sidx];
+  const int variant = scn.variant;
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
+  const int cap = RTC ? (int)min((int64_t)scn.num_accelerators * scn.models_per_accelerator, (int64_t)M) : C;
   // With capacity >= pool size every model fits: no eviction decision ever
   // happens, so the lookahead window is never read and is not maintained.
-  const bool warp_win = __any_sync(kFull, need_win) && C < M;
+  const bool warp_win = __any_sync(kFull, need_win) && cap > 1 && cap < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{l_p4f + threadIdx.x, l_p4d + threadIdx.x, l_slot + threadIdx.x, l_prm + threadIdx.x,
                    l_p4d + (size_t)M * LANE_BLOCK + threadIdx.x, nullptr, l_sof + threadIdx.x, LANE_BLOCK,
                    w_rec, w_win, w_samp, w_bar};
-  replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks, false, 1, MC>(P, sidx, shadow, warp_win, K, S);
+  replay_scenario<C, MW, DM, MINB != kLaneLatencyMinBlocks, false, 1, MC, RTC>(P, sidx, shadow, warp_win, K, S,
+                                                                             cap);
 }
 
 // ---- wide pools / capacities ----------------------------------------------
@@ -1203,7 +1216,7 @@ __global__ void __launch_bounds__(LANE_BLOCK_WIDE, 4) replay_lane_wide_kernel(Re
   // the warp's scenarios share the effective capacity (planner groups by it)
   const int cap = (int)min((int64_t)sc.num_accelerators * sc.models_per_accelerator, (int64_t)M);
   const bool need_win = variant != CACE_LRU && variant != CACE_MINUS_P3;
-  const bool warp_win = __any_sync(kFull, need_win) && cap < M;
+  const bool warp_win = __any_sync(kFull, need_win) && cap > 1 && cap < M;
   const CatShared K{s_lt, s_p2, s_tok, s_p2f, s_tokf, s_lex};
   const LaneSmem S{nullptr, nullptr, l_slot + col, l_prm + col, l_ud + col, l_wprm + col, l_sof + col, SB,
                    w_rec, w_win, w_samp, w_bar};

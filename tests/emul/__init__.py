@@ -34,11 +34,13 @@ def lib():
     return _lib
 
 
-def replay_batch(traces, catalog, scenarios, log_variant, dump=False, rolled_exact=True, wide=False):
+def replay_batch(traces, catalog, scenarios, log_variant, dump=False, rolled_exact=True, wide=False, mixed=False):
     """Host emulation of cace_replay_batch (summaries; optionally full dumps of
     every scenario).  wide=True runs every scenario through the wide-pool
     code path (runtime capacity, no per-lane p2 + p4 tables), which pools of
-    more than 64 models and capacities above 16 always take."""
+    more than 64 models and capacities above 16 always take; mixed=True runs
+    capacities <= 8 through the runtime-capacity one-lane path of the
+    mixed-capacity launch (shallow sweeps)."""
     from paper_2506_18796_b200 import _native as N
     from paper_2506_18796_b200.api import _trace_array
 
@@ -64,7 +66,7 @@ def replay_batch(traces, catalog, scenarios, log_variant, dump=False, rolled_exa
         args = [None, None, None, None, None, None, None, C.c_int64(0), None, None, None]
     rc = lib().emul_replay_batch(C.byref(catalog.abi()), C.cast(tarr, C.c_void_p), len(traces), p(sc),
                                  C.c_int64(len(sc)), p(out), C.c_int32(log_variant), *args,
-                                 C.c_int32(1 if rolled_exact else 0), C.c_int32(1 if wide else 0))
+                                 C.c_int32(1 if rolled_exact else 0), C.c_int32(2 if mixed else (1 if wide else 0)))
     if rc != 0:
         raise RuntimeError(f"emulation rc={rc}")
     return out, extra

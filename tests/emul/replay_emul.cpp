@@ -62,6 +62,24 @@ static void one(const ReplayParams& P, int64_t i, const CatShared& K) {
     replay_scenario<C, 2, D, false>(P, i, false, need_win, K, S);
 }
 
+// The mixed-capacity (runtime capacity <= 8) one-lane mode of shallow sweeps.
+template <bool D>
+static void one_rtc(const ReplayParams& P, int64_t i, const CatShared& K, int cap) {
+  const int v = P.scen[i].variant;
+  const bool need_win = v != CACE_LRU && v != CACE_MINUS_P3;
+  std::vector<float> p4f(P.cat.M), prm(4);
+  std::vector<double> p4d(P.cat.M + 1);
+  std::vector<SlotEnt> slot(8);
+  std::vector<uint8_t> slot_of(P.cat.M);
+  const LaneSmem S{p4f.data(), p4d.data(), slot.data(), prm.data(), p4d.data() + P.cat.M, nullptr, slot_of.data(),
+                   1, nullptr, nullptr, nullptr, nullptr};
+  const bool win = need_win && cap > 1 && cap < P.cat.M;
+  if (g_xr)
+    replay_scenario<8, 2, D, true, false, 1, 0, true>(P, i, false, win, K, S, cap);
+  else
+    replay_scenario<8, 2, D, false, false, 1, 0, true>(P, i, false, win, K, S, cap);
+}
+
 // The wide-pool mode (pools up to 256 models, capacity <= 32 at run time).
 template <bool D>
 static void one_wide(const ReplayParams& P, int64_t i, const CatShared& K, int cap) {
@@ -134,7 +152,11 @@ extern "C" int32_t emul_replay_batch(const cace_catalog_t* catalog, const cace_t
       }
       const int Cap = (int)effective_capacity(sc[i], cat.M);
       const bool D = dump_slot != nullptr;
-      if (wide || Cap > 16 || cat.M > 64) {  // the wide-pool lane kernel's code path
+      if (wide == 2 && Cap <= 8 && cat.M <= 64) {  // the mixed-capacity launch's code path
+        D ? one_rtc<true>(P, i, K, Cap) : one_rtc<false>(P, i, K, Cap);
+        continue;
+      }
+      if (wide == 1 || Cap > 16 || cat.M > 64) {  // the wide-pool lane kernel's code path
         if (Cap > 32 || cat.M > 256) return CACE_E_INVALID;
         D ? one_wide<true>(P, i, K, Cap) : one_wide<false>(P, i, K, Cap);
         continue;

@@ -140,3 +140,29 @@ def test_emulated_wide_path_small_pools(ref, emul, seed):
     rcat = ref_catalog(ref, catalog)
     want, _ = ref.run_batch(rcat, [ref_trace(t) for t in traces], [ref_scenario(ref, s) for s in sc])
     assert_summaries_equal(got, want, "wide path")
+
+
+@pytest.mark.parametrize("rolled", [True, False])
+def test_emulated_mixed_capacity_path(ref, emul, rolled):
+    """The runtime-capacity one-lane path of the mixed-capacity launch
+    (shallow sweeps: one kernel for every capacity <= 8) on the config-4 grid
+    shape and random scenarios, both exact-fallback variants, bit-exact
+    against the reference."""
+    from paper_2506_18796_b200 import api, synth
+    from paper_2506_18796_b200.api import ClusterConfig, PolicyConfig
+
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 6000, seed=s) for s in (3, 4)]
+    sc = synth.scenario_grid(synth.weight_vectors_cfg3()[::128], range(1, 9), 2, 600)
+    rng = np.random.default_rng(77)
+    rows = [(int(rng.integers(0, 2)),
+             PolicyConfig(variant=int(rng.integers(0, 6)), w1=float(rng.choice([0.0, 0.7, 1.7])),
+                          window_length=int(rng.choice([1, 4, 40])), p1_mode=int(rng.integers(0, 2))),
+             ClusterConfig(num_accelerators=int(rng.integers(1, 5)), models_per_accelerator=int(rng.integers(1, 3)),
+                           unload_time_s=float(rng.choice([0.0, 0.5]))))
+            for _ in range(24)]
+    sc = np.concatenate([sc, api.make_scenarios(rows)])
+    got, _ = emul.replay_batch(traces, catalog, sc, _logv(), rolled_exact=rolled, mixed=True)
+    want, _ = ref.run_batch(ref_catalog(ref, catalog), [ref_trace(t) for t in traces],
+                            [ref_scenario(ref, s) for s in sc])
+    assert_summaries_equal(got, want, "mixed-capacity path")

@@ -1,6 +1,6 @@
-# round-2: e2e overlap (trace DMA || plan || scenario upload) and pooled stream sets.
-OUT=gpurun_out; mkdir -p $OUT; TAG=r2v
+# round-2: shallow-sweep policy (mixed launch at MINB 4 below 1.5 waves) on the default library; tests.
+OUT=gpurun_out; mkdir -p $OUT; TAG=r2z
 timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 900 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_$TAG.log
-CACE_TIMING=1 timeout 600 python tools/e2e_timing.py > $OUT/e2e_timing_$TAG.log 2>&1
-timeout 900 python bench.py --steps 5 --warmup 3 --e2e-steps 4 --parity-sample 64 --cpu-sample 16 > $OUT/bench_cfg4_$TAG.log 2>&1
-timeout 600 python tools/sanitize_run.py > $OUT/sanitize_plain_$TAG.log 2>&1; echo "rc=$?" >> $OUT/sanitize_plain_$TAG.log
+for s in 32 16 8 4; do timeout 900 python bench.py --seeds $s --steps 5 --warmup 3 --parity-sample 256 --cpu-sample 32 > $OUT/bench_s${s}_$TAG.log 2>&1; done
+timeout 900 python bench.py --config 3 --steps 5 --warmup 3 --parity-sample 256 > $OUT/bench_cfg3_$TAG.log 2>&1
+AB_ARGS="--seeds 4;--seeds 2;--seeds 1" bash tools/gpu_ab_env.sh ${TAG} "" "CACE_MIXED=0"
