@@ -1103,7 +1103,9 @@ int32_t cace_run_metrics_batch(const cace_catalog_t* catalog, const cace_trace_t
     // buffer is reused in stream order while the other streams keep the SMs
     // full of replay lanes.  Chunk-local arrays are concatenated in chunk
     // order (position p = chunk base + local index).
-    const size_t W = e->workers.size();
+    size_t W = e->workers.size();
+    if (const char* v = std::getenv("CACE_METRICS_RINGS"))  // tuning override (1..8)
+      W = std::max<size_t>(1, std::min<size_t>(W, (size_t)std::atoi(v)));
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     // memory the stream-ordered pool holds but does not use is free to us

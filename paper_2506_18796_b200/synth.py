@@ -114,7 +114,8 @@ def config5(n_requests: int = 10_000_000, n_scenarios: int = 8192, capacity: int
             trace_seed: int = 1):
     """BASELINE config 5: 256 CodeLLMs, one bursty (MMPP) trace, long window,
     capacity 32; scenarios = w1 x {cace, -p1, -p2, -p4} x P1 mode x unload
-    delay (n_scenarios of that grid).  Needs the warp-per-scenario kernel."""
+    delay (n_scenarios of that grid).  Runs on the wide-pool lane kernel (8 lanes
+    per scenario)."""
     catalog = ModelCatalog.synthetic_pool(256, seed=5)
     traces = [mixed_trace(catalog, n_requests, seed=trace_seed, rate=40.0, bursty=True)]
     rows = []
