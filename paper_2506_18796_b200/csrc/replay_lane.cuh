@@ -683,9 +683,11 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
             const float p2s = WIDE ? S.wprm[0] : 0.0f, p4s = WIDE ? S.wprm[st] : 0.0f;
             float best = -INFINITY, second = -INFINITY;
             int bs = 0;
+            float Ts[C];  // screened totals (the exact pass skips the hopeless ones)
             const uint32_t wend = k + w;
 #pragma unroll
             for (int s = 0; s < C; ++s) {
+              Ts[s] = -INFINITY;
               if ((WIDE || RTC) && s >= cap) break;
               const int ms = slot_model(sw[s]);
               const float t = fmaxf((float)(now - sd[s]), 1.0f);  // max(d, 1) in fp32
@@ -699,13 +701,33 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               float T = (p1 + p3) + (WIDE ? fmaf(p4s, K.tokf[ms], p2s * K.p2f[ms])
                                           : S.p4f[ms * st]);  // p2 + p4 pre-summed
               T = ((idm >> s) & 1u) ? T : -INFINITY;
+              Ts[s] = T;
               bs = T > best ? s : bs;
               second = fmaxf(second, fminf(best, T));
               best = fmaxf(best, T);
             }
             v = bs;
-            if (!(best - second > S.prm[3 * st])) {
+            const float margin = S.prm[3 * st];
+            if (!(best - second > margin)) {
               CACE_STAT(5, k);
+              // Only candidates whose screened total is within the margin of
+              // the best can be the exact arg-max: every screened total is
+              // within margin / 2 of its exact value, so T_s < best - margin
+              // means exact_s < exact_best.  (No pruning when the screen is
+              // off -- infinite margin, possibly non-finite totals.)
+              // Measured: +4% on deep sweeps (per-capacity, rolled exact
+              // path); -2..-5% in the latency (unrolled) and mixed-capacity
+              // instantiations, which keep the full candidate set.
+              constexpr bool kPrune = XR && !RTC;
+              unsigned idx = idm;
+              if (kPrune) {
+                const float thr = margin < INFINITY ? best - margin : -INFINITY;
+                unsigned near = 0;
+#pragma unroll
+                for (int s = 0; s < C; ++s)
+                  if (!(Ts[s] < thr)) near |= 1u << s;
+                idx &= near;
+              }
               // Exact fp64 eviction_score (policy.cpp:39-78) and "first
               // strict max in (last_used, model_id) order"
               // (policy.cpp:92-113), bit-identical to the reference; taken on
@@ -750,14 +772,14 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               unsigned nanm = 0;
               if constexpr (XR) {
 #pragma unroll 1
-                for (unsigned q = idm; q; q &= q - 1u) {
+                for (unsigned q = idx; q; q &= q - 1u) {
                   const int s = __ffs(q) - 1;
                   if (cand(s, S.slot[s * st].done, S.slot[s * st].word)) nanm |= 1u << s;
                 }
               } else {
 #pragma unroll
                 for (int s = 0; s < C; ++s)
-                  if ((idm >> s) & 1u)
+                  if ((idx >> s) & 1u)
                     if (cand(s, sd[s], sw[s])) nanm |= 1u << s;
               }
               f_nan = (nanm >> f) & 1u;
