@@ -1,3 +1,3 @@
-# round-2: exact-fallback pruning only in the rolled per-capacity instantiations.
-OUT=gpurun_out; mkdir -p $OUT; TAG=r2ae
-AB_ARGS="--seeds 32;--seeds 16;--seeds 8;--seeds 4;--config 3" bash tools/gpu_ab_libs.sh ${TAG} default _variants/libcace_base.so
+# round-2: p1 shared by exact candidates with equal last_used.
+OUT=gpurun_out; mkdir -p $OUT; TAG=r2af
+AB_ARGS="--seeds 32;--seeds 8;--seeds 4;--config 3" bash tools/gpu_ab_libs.sh ${TAG} default _variants/libcace_base.so default _variants/libcace_base.so
