@@ -777,10 +777,49 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               };
               unsigned nanm = 0;
               if constexpr (XR) {
+                // Exact-tie shortcut: when every remaining candidate has the
+                // same last_used (so the same p1), p3 = 1 (first pending
+                // request outside the window or not arrived) and the same p2
+                // and p4, all exact totals are bitwise equal and the reference
+                // keeps the first in (last_used, model_id) order: the least
+                // lex rank.  (Same-class models of a pool share load time and
+                // expected tokens; same-time completions share last_used.)
+                bool tie = kPrune;
+                double lu0 = 0.0, p20 = 0.0, p40 = 0.0;
+                int tlex = 0x7fffffff, ts = -1;
 #pragma unroll 1
-                for (unsigned q = idx; q; q &= q - 1u) {
+                for (unsigned q = idx; tie && q; q &= q - 1u) {
                   const int s = __ffs(q) - 1;
-                  if (cand(s, S.slot[s * st].done, S.slot[s * st].word)) nanm |= 1u << s;
+                  const double lu = S.slot[s * st].done;
+                  const int wd = S.slot[s * st].word;
+                  const int ms = slot_model(wd);
+                  const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
+                  const double p4 = S.p4d[ms * st];
+                  bool p3one = true;
+                  if (variant != CACE_MINUS_P3) {
+                    const WinEnt e = win.gather(ms);
+                    p3one = !(e.f - k < w && e.fa < now);
+                  }
+                  if (ts < 0) {
+                    lu0 = lu;
+                    p20 = p2;
+                    p40 = p4;
+                  }
+                  tie = p3one && lu == lu0 && p2 == p20 && p4 == p40;
+                  if (slot_lex(wd) < tlex) {
+                    tlex = slot_lex(wd);
+                    ts = s;
+                  }
+                }
+                if (tie) {
+                  f = ts;  // sorted-first; no NaN with the screen on
+                  bv = ts;
+                } else {
+#pragma unroll 1
+                  for (unsigned q = idx; q; q &= q - 1u) {
+                    const int s = __ffs(q) - 1;
+                    if (cand(s, S.slot[s * st].done, S.slot[s * st].word)) nanm |= 1u << s;
+                  }
                 }
               } else {
 #pragma unroll
