@@ -1,9 +1,5 @@
-# round-2: full verification of the current library: tests, smoke, sanitizers, default bench, configs 3/5, shards.
-OUT=gpurun_out; mkdir -p $OUT; TAG=r2ag
+# round-2: validate the exact-tie shortcut build; ncu of the C = 6 and C = 3 launches.
+OUT=gpurun_out; mkdir -p $OUT; TAG=r2ai
 timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 900 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_$TAG.log
-timeout 300 python __graft_entry__.py smoke > $OUT/smoke_$TAG.log 2>&1; echo "rc=$?" >> $OUT/smoke_$TAG.log
-for t in racecheck memcheck; do timeout 1200 compute-sanitizer --tool $t --error-exitcode 9 python tools/sanitize_run.py > $OUT/sanitize_${t}_$TAG.log 2>&1; echo "rc=$?" >> $OUT/sanitize_${t}_$TAG.log; done
-timeout 900 python bench.py > $OUT/bench_cfg4_$TAG.log 2>&1
-timeout 900 python bench.py --config 3 --steps 5 --warmup 3 --parity-sample 256 > $OUT/bench_cfg3_$TAG.log 2>&1
-for s in 16 8 4; do timeout 900 python bench.py --seeds $s --steps 5 --warmup 3 --parity-sample 256 --cpu-sample 32 > $OUT/bench_s${s}_$TAG.log 2>&1; done
-timeout 1500 python bench.py --config 5 --steps 2 --warmup 3 --e2e-steps 1 --parity-sample 16 --cpu-sample 8 > $OUT/bench_cfg5_$TAG.log 2>&1
+bash tools/gpu_ncu.sh ${TAG}_C6 "replay_lane_kernel<.int.6," --parity-sample 0
+bash tools/gpu_ncu.sh ${TAG}_C3 "replay_lane_kernel<.int.3," --parity-sample 0
