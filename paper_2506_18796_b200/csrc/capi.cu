@@ -328,11 +328,16 @@ void finish_upload(cace_engine* e) {
   e->upload_pending = false;
   decltype(e->lay.rec)().swap(e->lay.rec);  // device copy is authoritative
   e->lay.ext_rec = nullptr;
-  std::vector<uint32_t>().swap(e->lay.perm);
   if (e->arena_held) {
     g_arena.release();
     e->arena_held = false;
   }
+}
+
+// Device copy of the replay-order -> caller-order permutation, for dumps.
+void ensure_perm(cace_engine* e) {
+  if (e->d_perm.p || e->lay.perm.empty()) return;
+  e->d_perm.upload(e->lay.perm.data(), e->lay.perm.size(), e->stream);
 }
 
 void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trace_t* traces,
@@ -383,7 +388,8 @@ void build_engine(cace_engine* e, const cace_catalog_t* catalog, const cace_trac
   e->d_rec.upload(e->lay.records(), (size_t)e->lay.off[e->lay.T], s);
   e->d_off.upload(e->lay.off.data(), e->lay.off.size(), s);
   e->d_first0.upload(e->lay.first0.data(), e->lay.first0.size(), s);
-  e->d_perm.upload(e->lay.perm.data(), e->lay.perm.size(), s);
+  // the permutation back to caller order only serves full dumps: uploaded
+  // on first use (ensure_perm)
   e->d_ncomp.upload(e->lay.ncomp.data(), e->lay.ncomp.size(), s);
   e->d_tab.upload(kLogTab, 256, s);
   e->d_tab2.upload(kLogTab2, 256, s);
@@ -971,6 +977,7 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
     int64_t total = 0;
     const int nd = dump ? dump->n_dump : 0;
     if (nd > 0) {
+      ensure_perm(e);
       std::vector<int32_t> slot(n_scenarios, -1);
       for (int k = 0; k < nd; ++k) {
         const int64_t si = dump->scenario_index[k];
