@@ -922,10 +922,12 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               const float p2s = S.wprm[0], p4s = S.wprm[st];
               float best = -INFINITY, second = -INFINITY;
               int bs = 0x7fffffff;
+              float Tj[J];  // the lane's screened totals (exact-pass pruning)
               const uint32_t wend = k + w;
 #pragma unroll
               for (int j = 0; j < J; ++j) {
                 const int s = lig + G * j;
+                Tj[j] = -INFINITY;
                 if (!((idm >> s) & 1u)) continue;
                 const int ms = slot_model(lwd[j]);
                 const float t = fmaxf((float)(now - ld[j]), 1.0f);  // max(d, 1) in fp32
@@ -937,6 +939,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                   p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
                 }
                 const float T = (p1 + p3) + fmaf(p4s, K.tokf[ms], p2s * K.p2f[ms]);
+                Tj[j] = T;
                 bs = T > best ? s : bs;
                 second = fmaxf(second, fminf(best, T));
                 best = fmaxf(best, T);
@@ -951,25 +954,44 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 best = fmaxf(best, ob);
               }
               v = bs;
-              if (!(best - second > S.prm[3 * st])) {
+              const float margin = S.prm[3 * st];
+              if (!(best - second > margin)) {
                 // exact fp64 path (policy.cpp:39-78, 92-113): every lane of
-                // the group walks all idle slots (identical result, no reduction)
+                // the group walks the idle slots (identical result, no
+                // reduction) -- only those whose screened total is within the
+                // margin of the best (the group ORs its lanes' masks; no
+                // pruning with the screen off), one glibc log per distinct
+                // last_used
+                unsigned idx = idm;
+                if (margin < INFINITY) {
+                  const float thr = best - margin;
+                  unsigned near = 0;
+#pragma unroll
+                  for (int j = 0; j < J; ++j)
+                    if (!(Tj[j] < thr)) near |= 1u << (lig + G * j);
+#pragma unroll
+                  for (int o = 1; o < G; o <<= 1) near |= __shfl_xor_sync(gmask, near, o);
+                  idx &= near;
+                }
                 int f = -1;
                 double flu = 0.0;
                 int flex = 0;
                 double bt = 0.0, blu = 0.0;
                 int blex = 0, bv = -1;
                 bool f_nan = false;
+                double c_lu = -1.0, c_p1 = 0.0;
 #pragma unroll 1
-                for (unsigned q = idm; q; q &= q - 1u) {
+                for (unsigned q = idx; q; q &= q - 1u) {
                   const int s = __ffs(q) - 1;
                   const double lu = S.slot[s * st].done;
                   const int wd = S.slot[s * st].word;
                   const int ms = slot_model(wd);
                   const int lx = slot_lex(wd);
-                  const double p1 = variant == CACE_MINUS_P1
-                                        ? 0.0
-                                        : exact_p1(now, lu, verbatim, P.log_variant, P.log_tab, P.log_tab2);
+                  if (variant != CACE_MINUS_P1 && lu != c_lu) {
+                    c_lu = lu;
+                    c_p1 = exact_p1(now, lu, verbatim, P.log_variant, P.log_tab, P.log_tab2);
+                  }
+                  const double p1 = variant == CACE_MINUS_P1 ? 0.0 : c_p1;
                   const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
                   double p3 = 0.0;
                   if (variant != CACE_MINUS_P3) {
