@@ -171,6 +171,7 @@ struct Window {
     }
   }
   WinEnt gather(int ms) const { return WinEnt{f[ms], (float)r[ms], fa[ms]}; }
+  WinEnt gather128(int ms) const { return gather(ms); }
   int pmk = 0;
   uint32_t pnx = 0;
   void prepare(int mk, uint32_t nx) {
@@ -214,6 +215,13 @@ struct Window {
   }
   // Per lane (no collective): model ms's entry.
   __device__ __forceinline__ WinEnt gather(int ms) const { return tab[ms]; }
+  // The same entry through one 128-bit load: +3% on the wide-pool kernel
+  // (config 5), -5% on the latency instantiation (config 3), so only the
+  // wide mode uses it (profiles/r2/ab_window_load_r2am.txt).
+  __device__ __forceinline__ WinEnt gather128(int ms) const {
+    const uint4 q = *reinterpret_cast<const uint4*>(tab + ms);
+    return WinEnt{q.x, __uint_as_float(q.y), __hiloint2double((int)q.w, (int)q.z)};
+  }
   // Collective: prepare computes the state after the head (model mk) is
   // served -- mk's first becomes nx -- without touching what the iteration's
   // decisions read; commit installs it.  (Issuing prepare at the top of the
@@ -935,7 +943,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                 const float p1 = fmaf(p1s, p1v, p1o);
                 float p3 = 0.0f;
                 if (need_win) {
-                  const WinEnt e = win.gather(ms);
+                  const WinEnt e = win.gather128(ms);
                   p3 = (e.f < wend && e.fa < now) ? e.r * rcpw : 1.0f;
                 }
                 const float T = (p1 + p3) + fmaf(p4s, K.tokf[ms], p2s * K.p2f[ms]);
@@ -995,7 +1003,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
                   const double p2 = variant == CACE_MINUS_P2 ? 0.0 : K.p2[ms];
                   double p3 = 0.0;
                   if (variant != CACE_MINUS_P3) {
-                    const WinEnt e = win.gather(ms);
+                    const WinEnt e = win.gather128(ms);
                     p3 = (e.f - k < w && e.fa < now) ? (double)e.r / (double)w : 1.0;
                   }
                   const double p4 = variant == CACE_MINUS_P4 ? 0.0 : sc.w1 * (K.tok[ms] / norm);
