@@ -726,7 +726,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               // Measured: +4% on deep sweeps (per-capacity, rolled exact
               // path); -2..-5% in the latency (unrolled) and mixed-capacity
               // instantiations, which keep the full candidate set.
-              constexpr bool kPrune = XR && !RTC;
+              constexpr bool kPrune = XR && !RTC;  // mixed-capacity: -15% with it (ab_rtc_prune_r2ao)
               unsigned idx = idm;
               if (kPrune) {
                 const float thr = margin < INFINITY ? best - margin : -INFINITY;
