@@ -41,18 +41,21 @@
 // m needs first[m] (first replay index >= k requesting m), rank(m) =
 // #{m' : first[m'] < first[m]} and whether first[m] has arrived.  These
 // depend only on the trace and k, so they are warp-wide: lane j owns models
-// j, j+32 in registers, advances them with one ballot/popc per request and
+// j, j+32 in registers, advances them with one warp reduction per request and
 // publishes {first, rank, arrival of first} to a per-warp shared-memory table
-// that deciding lanes read with one 128-bit load per candidate.
+// that deciding lanes read per candidate.
 //
-// The trace is staged per warp in shared memory by cp.async (32-record
-// chunks, double-buffered), so the per-request record read is a broadcast
-// shared load and no registers carry a prefetched record.
+// The trace is staged per warp in shared memory by TMA bulk copies (one
+// cp.async.bulk of 32 records per chunk, double-buffered, mbarrier-completed),
+// so the per-request record read is a broadcast shared load and no registers
+// carry a prefetched record.
 //
 // All fp64 arithmetic uses the reference's operation order with no
 // contraction (built with -fmad=false); P1's log is the glibc restatement
 // (glibc_log.cuh).  Decisions are first screened in fp32 with a rigorous
-// error margin; near-ties fall back to the exact fp64 scores.
+// error margin; near-ties fall back to the exact fp64 scores of the
+// candidates within the margin (exact ties of identical inputs short-cut to
+// the reference's tie order).
 #pragma once
 #include <math.h>
 #include <stdint.h>
