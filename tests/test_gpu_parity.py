@@ -387,3 +387,22 @@ def test_reference_side_binding_drop_in():
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ADAPTER ALL_OK" in out.stdout
+
+
+def test_mixed_capacity_launch_matches_per_capacity(ref, monkeypatch):
+    """Shallow sweeps (0.5-1.5 waves of lane warps, several capacities) run as
+    ONE mixed-capacity launch of the runtime-capacity instantiation; its
+    summaries equal the per-capacity launches byte for byte (CACE_MIXED=0) and
+    a stratified sample equals the reference."""
+    catalog = synth.eight_model_catalog()
+    traces = [synth.mixed_trace(catalog, 1500, seed=60 + s) for s in range(2)]
+    # 4096 vectors x 8 capacities x 2 traces = 65536 scenarios = 2048 lane warps (~0.7 waves)
+    sc = synth.scenario_grid(synth.weight_vectors_cfg3(), range(1, 9), 2, catalog.max_expected_output_tokens())
+    mixed = P.run_batch(traces, catalog, sc)
+    monkeypatch.setenv("CACE_MIXED", "0")
+    per_cap = P.run_batch(traces, catalog, sc)
+    assert mixed.tobytes() == per_cap.tobytes()
+    pick = np.random.default_rng(9).choice(len(sc), 48, replace=False)
+    want, _ = ref.run_batch(ref_catalog(ref, catalog), [ref_trace(t) for t in traces],
+                            [ref_scenario(ref, s) for s in sc[pick]])
+    assert_summaries_equal(mixed[pick], want, "mixed-capacity launch")
