@@ -418,8 +418,29 @@ struct LaneSmem {
 // last_used_s = done -- iff its key is <= the cursor.
 constexpr uint32_t kKindSC = 1u << 30;
 constexpr uint32_t kKindArr = 2u << 30;
+// Compared as 96-bit unsigned keys (bits(done), kKindSC | seq) <=
+// (bits(ct), cw): every clock value is a non-negative finite double
+// (layout.hpp rejects negative arrivals; done = (now + pf) + dc is never -0)
+// whose bit pattern orders like the value, and the cursor's sign bit is
+// cleared so an arrival at -0.0 compares equal to +0.0.  One integer
+// subtract-with-borrow chain instead of two fp64 compares.
 __device__ __forceinline__ bool sc_popped(double done, uint32_t seq, double ct, uint32_t cw) {
-  return done < ct || (done == ct && (kKindSC | seq) <= cw);
+  const uint64_t db = (uint64_t)__double_as_longlong(done);
+  const uint64_t cb = (uint64_t)__double_as_longlong(ct) & 0x7fffffffffffffffull;
+#ifdef CACE_HOST_EMULATION
+  return db < cb || (db == cb && (kKindSC | seq) <= cw);
+#else
+  uint32_t b;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "sub.cc.u32 t, %1, %2;\n\t"
+      "subc.cc.u32 t, %3, %4;\n\t"
+      "subc.cc.u32 t, %5, %6;\n\t"
+      "subc.u32 %0, 0, 0;\n\t}"
+      : "=r"(b)
+      : "r"(cw), "r"(kKindSC | seq), "r"((uint32_t)cb), "r"((uint32_t)db), "r"((uint32_t)(cb >> 32)),
+        "r"((uint32_t)(db >> 32)));
+  return b == 0u;
+#endif
 }
 
 // Metrics samples leave through a per-warp shared tile: the lanes of a warp

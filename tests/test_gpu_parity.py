@@ -153,6 +153,23 @@ def test_unsorted_trace_and_equal_arrivals(ref):
     _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "unsorted")
 
 
+def test_negative_zero_arrivals(ref):
+    """Arrivals at -0.0 pass the reference's `< 0` check; the event cursor
+    compares clock bit patterns with the sign bit cleared, so -0.0 and +0.0
+    must behave as the same instant (engine.cpp:49-55)."""
+    catalog = synth.eight_model_catalog()
+    rng = np.random.default_rng(9)
+    n = 400
+    arr = np.sort(np.round(rng.uniform(0, 20, n), 0))
+    arr[:40] = 0.0
+    arr[:40:2] = -0.0  # interleaved signed zeros among the first arrivals
+    assert np.signbit(arr).sum() == 20
+    t = api.Trace(arr, rng.integers(0, 8, n), rng.integers(0, 300, n), rng.integers(0, 40, n))
+    rows = [(0, PolicyConfig(variant=v, window_length=w), ClusterConfig(num_accelerators=c))
+            for v in range(6) for w in (1, 5) for c in (1, 2, 3, 5)]
+    _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "negzero")
+
+
 def test_simultaneous_completions_push_order(ref):
     """Same-time ServiceCompletes must pop in push (seq) order (engine.cpp:49-55)."""
     catalog = synth.eight_model_catalog()
