@@ -516,9 +516,10 @@ def main():
     if args.kernel == "warp" or len(catalog) > 256:
         kernel = "replay_warp_kernel<SPL> (warp per scenario)"
     elif len(catalog) > 64:
-        kernel = "replay_lane_wide_kernel<MW,DM> (lane per scenario, wide pools, one warp per block)"
+        kernel = "replay_lane_wide_kernel<MW,DM,G> (G = 8 lanes per scenario, wide pools)"
     else:
-        kernel = "replay_lane_kernel<C,...> (one launch per capacity segment, run concurrently)"
+        kernel = ("replay_lane_kernel<C,...> (one launch per capacity segment, run concurrently; "
+                  "0.5-1.5-wave sweeps of several capacities: one mixed-capacity launch)")
     out = {
         "metric": "scenario-requests replayed/sec", "value": value, "unit": "scenario-requests/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max,
