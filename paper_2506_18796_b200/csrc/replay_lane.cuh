@@ -424,7 +424,11 @@ constexpr uint32_t kKindArr = 2u << 30;
 // whose bit pattern orders like the value, and the cursor's sign bit is
 // cleared so an arrival at -0.0 compares equal to +0.0.  One integer
 // subtract-with-borrow chain instead of two fp64 compares.
+// The wide-pool kernel keeps the two fp64 compares (INTKEY = false): there
+// the integer chain measured 6% slower on config 5 (profiles/r2/ab_wide_key_r2ba.txt).
+template <bool INTKEY = true>
 __device__ __forceinline__ bool sc_popped(double done, uint32_t seq, double ct, uint32_t cw) {
+  if constexpr (!INTKEY) return done < ct || (done == ct && (kKindSC | seq) <= cw);
   const uint64_t db = (uint64_t)__double_as_longlong(done);
   const uint64_t cb = (uint64_t)__double_as_longlong(ct) & 0x7fffffffffffffffull;
 #ifdef CACE_HOST_EMULATION
@@ -628,7 +632,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
       const SlotEnt te = S.slot[hs * st];  // one 16-B load
       const double td = te.done;
       const uint32_t tq = te.seq;
-      if (!sc_popped(td, tq, ct, cw)) {
+      if (!sc_popped<!WIDE>(td, tq, ct, cw)) {
         ct = td;
         cw = kKindSC | tq;
       }
@@ -654,7 +658,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
           sd[s] = e.done;
           sq[s] = e.seq;
           sw[s] = e.word;
-          idm |= sc_popped(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
+          idm |= sc_popped<!WIDE>(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
         }
         if (idm == 0) {
           // every resident busy: nothing to evict now (select_victim ->
@@ -884,7 +888,7 @@ __device__ void replay_scenario(const ReplayParams& P, int64_t sidx, bool shadow
               ld[j] = e.done;
               lq[j] = e.seq;
               lwd[j] = e.word;
-              idm |= sc_popped(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
+              idm |= sc_popped<!WIDE>(e.done, e.seq, ct, cw) ? (1u << s) : 0u;
             }
           }
 #pragma unroll
