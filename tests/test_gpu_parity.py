@@ -170,6 +170,22 @@ def test_negative_zero_arrivals(ref):
     _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "negzero")
 
 
+def test_extreme_clock_magnitudes(ref):
+    """The cursor test orders clocks by their bit patterns: subnormal, tiny and
+    huge arrivals (where service times round away and completions tie
+    exactly) must replay as the reference's fp64 comparisons do."""
+    catalog = synth.eight_model_catalog()
+    rng = np.random.default_rng(13)
+    n = 480
+    arr = np.sort(np.concatenate([
+        np.array([0.0, 5e-324, 1e-320, 2.2250738585072014e-308, 1e-300]),
+        rng.uniform(0, 1e-6, 95), rng.uniform(1, 100, 190), 1e15 + np.round(rng.uniform(0, 64, 190))]))
+    t = api.Trace(arr, rng.integers(0, 8, n), rng.integers(1, 400, n), rng.integers(0, 60, n))
+    rows = [(0, PolicyConfig(variant=v, window_length=w), ClusterConfig(num_accelerators=c))
+            for v in range(6) for w in (1, 6) for c in (2, 3, 5)]
+    _replay_and_compare(ref, catalog, [t], api.make_scenarios(rows), "extreme")
+
+
 def test_simultaneous_completions_push_order(ref):
     """Same-time ServiceCompletes must pop in push (seq) order (engine.cpp:49-55)."""
     catalog = synth.eight_model_catalog()
