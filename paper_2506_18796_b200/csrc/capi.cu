@@ -1064,10 +1064,13 @@ int32_t cace_replay_batch(const cace_catalog_t* catalog, const cace_trace_t* tra
     CK(cudaStreamSynchronize(s));
     if (stage) par_memcpy(summaries, stage, sbytes);
     pt.mark("download");
-    for (int64_t i = 0; i < n_scenarios; ++i) {
-      if (summaries[i].status != CACE_OK) {
-        put_msg(msg, msg_cap, status_text(e->cat, summaries[i].status));
-        return summaries[i].status & 0xff;
+    // The replay kernels write CACE_OK; the only other statuses are the
+    // plan's precheck codes (fill_status), recorded in caller order -- no
+    // scan of the 112-B summaries (~6 ms for a 1M sweep).
+    for (size_t j = 0; j < e->bad_code.size(); ++j) {
+      if (e->bad_code[j] != CACE_OK) {
+        put_msg(msg, msg_cap, status_text(e->cat, e->bad_code[j]));
+        return e->bad_code[j] & 0xff;
       }
     }
     return CACE_OK;

@@ -1,3 +1,5 @@
-# round-2: parity file incl. the signed-zero and extreme-magnitude clock tests on the final library
-OUT=gpurun_out; mkdir -p $OUT; TAG=r2bd
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -rf > $OUT/pytest_parity_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_parity_$TAG.log
+# round-2: first-error status from the plan's precheck codes instead of a scan of the summaries (e2e)
+OUT=gpurun_out; mkdir -p $OUT; TAG=r2be
+timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 900 > $OUT/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_$TAG.log
+CACE_TIMING=1 timeout 600 python tools/e2e_timing.py > $OUT/e2e_timing_$TAG.log 2>&1
+timeout 900 python bench.py > $OUT/bench_cfg4_$TAG.log 2>&1
