@@ -270,6 +270,7 @@ struct cace_engine {
   // shallow sweeps: the lane segments of capacity <= kMixedC concatenated
   // heaviest first, replayed by ONE mixed-capacity launch (d_mixed)
   int64_t n_mixed = 0;
+  bool mixed_ready = false;  // d_mixed holds this plan's entries
   DBuf<int64_t> d_mixed;
   std::vector<int64_t> bad_idx;
   std::vector<int32_t> bad_code;
@@ -530,14 +531,12 @@ void plan(cace_engine* e, const cace_scenario_t* sc, int64_t n) {
   // per-capacity launches of a few hundred blocks each leave SMs unevenly
   // loaded (a 2560-warp sweep: 151 ms as five concurrent launches, 92 ms as
   // one; profiles/r2/ab_concurrency_r2w.txt).
-  {
-    std::vector<int64_t> mixed;
-    for (auto& g : e->segs) {
-      g.mixed = !g.warp && !g.wide && g.C <= kMixedC;
-      if (g.mixed) mixed.insert(mixed.end(), order.begin() + g.b, order.begin() + g.e);
-    }
-    e->n_mixed = (int64_t)mixed.size();
-    e->d_mixed.upload(mixed.data(), mixed.size(), e->stream);
+  // (its entry list is built and uploaded by replay() only when it is chosen)
+  e->n_mixed = 0;
+  e->mixed_ready = false;
+  for (auto& g : e->segs) {
+    g.mixed = !g.warp && !g.wide && g.C <= kMixedC;
+    if (g.mixed) e->n_mixed += g.e - g.b;
   }
   e->d_order.upload(order.data(), order.size(), e->stream);
   e->d_bad_idx.upload(e->bad_idx.data(), e->bad_idx.size(), e->stream);
@@ -786,6 +785,15 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
     if (nl > 1) fork_workers(e, s, nl);
     size_t k = 0;
     if (mixed) {
+      if (!e->mixed_ready) {
+        std::vector<int64_t> ent;
+        ent.reserve((size_t)e->n_mixed);
+        for (const auto& g : e->segs)
+          if (g.mixed) ent.insert(ent.end(), e->h_order.begin() + g.b, e->h_order.begin() + g.e);
+        e->d_mixed.upload(ent.data(), ent.size(), s);
+        CK(cudaStreamSynchronize(s));  // pageable source
+        e->mixed_ready = true;
+      }
       cudaStream_t ws = nl == 1 ? s : e->workers[k++ % e->workers.size()];
       ReplayParams Q = P;
       Q.order = e->d_mixed.p;
