@@ -63,6 +63,22 @@ def test_multi_device_errors_surface(ref):
         P.run_batch(traces, catalog, sc[:64], devices=[0, 99])
 
 
+@pytest.mark.parametrize("devices", [None, [0, 0]])
+def test_first_failing_scenario_in_caller_order_is_reported(devices):
+    """With several invalid scenarios the error is the first one in the
+    caller's order (the reference's run_grid loop raises at the first), on the
+    single- and the multi-device entry."""
+    catalog, traces, sc = _sweep()
+    kw = {} if devices is None else {"devices": devices}
+    for first, second, msg in (("unload_time_s", "window_length", "unload_time_s must be in"),
+                               ("window_length", "unload_time_s", "window_length must be >= 1")):
+        bad = sc[:256].copy()
+        bad[first][37] = -1.0 if first == "unload_time_s" else 0
+        bad[second][200] = -1.0 if second == "unload_time_s" else 0
+        with pytest.raises(P.SimError, match=msg):
+            P.run_batch(traces, catalog, bad, **kw)
+
+
 _RANK_WORKER = r"""
 import os, sys
 import numpy as np, torch, torch.distributed as dist
