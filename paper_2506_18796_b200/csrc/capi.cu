@@ -755,15 +755,16 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   const size_t nseg = e->segs.size();
   // Occupancy tier by sweep depth in waves of 20-warp-per-SM lane warps:
   // < 1.5 waves the step is one warp's dependency chain (register-rich
-  // MINB 3), 1.5-4.5 waves MINB 4, deeper sweeps are issue-bound (MINB 5).
-  // Measured on config-4 shards (131k / 262k / 524k / 1M scenarios).
+  // MINB 3), 1.5-2.5 waves MINB 4, deeper sweeps are issue-bound (MINB 5).
+  // Measured on config-4 shards (131k .. 1M scenarios; the 2.5 crossover on
+  // the final kernels: profiles/r2/ab_tiers_r2bm.txt).
   int64_t lane_warps = 0;
   for (const auto& g : e->segs)
     if (!g.warp) lane_warps += (g.e - g.b) / 32;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
   const double waves = (double)lane_warps / ((double)sms * (CACE_LANE_MIN_BLOCKS * 4));
-  int minb = waves < 1.5 ? kLaneLatencyMinBlocks : (waves < 4.5 ? kLaneMidMinBlocks : CACE_LANE_MIN_BLOCKS);
+  int minb = waves < 1.5 ? kLaneLatencyMinBlocks : (waves < 2.5 ? kLaneMidMinBlocks : CACE_LANE_MIN_BLOCKS);
   if (const char* v = std::getenv("CACE_LANE_MINB")) minb = std::atoi(v);  // tuning override (3, 4, 5)
   // From 0.5 to 1.5 waves with several capacities (a strong-scaling shard), the
   // capacities <= 8 run as ONE mixed-capacity launch at MINB 4 (summaries,
