@@ -766,14 +766,15 @@ void replay(cace_engine* e, const cace_scenario_t* d_sc, int64_t n, cace_summary
   const double waves = (double)lane_warps / ((double)sms * (CACE_LANE_MIN_BLOCKS * 4));
   int minb = waves < 1.5 ? kLaneLatencyMinBlocks : (waves < 2.5 ? kLaneMidMinBlocks : CACE_LANE_MIN_BLOCKS);
   if (const char* v = std::getenv("CACE_LANE_MINB")) minb = std::atoi(v);  // tuning override (3, 4, 5)
-  // From 0.5 to 1.5 waves with several capacities (a strong-scaling shard), the
+  // From 0.5 to 1.8 waves with several capacities (a strong-scaling shard), the
   // capacities <= 8 run as ONE mixed-capacity launch at MINB 4 (summaries,
   // pools <= 32 models): 131k shard 8.6e10 -> 1.21e11; at 262k the
   // per-capacity launches stay faster, and below 0.5 waves (32k scenarios)
-  // the per-capacity MINB 3 kernels (profiles/r2/ab_mixed_r2y.txt, ab_mixed_r2z.txt).
+  // the per-capacity MINB 3 kernels (profiles/r2/ab_mixed_r2y.txt, ab_mixed_r2z.txt);
+  // 1.73 waves (164k): mixed +7%, 2.08 waves (196k): -9% (ab_mixed_upper_r2bp.txt).
   int n_mixable = 0;
   for (const auto& g : e->segs) n_mixable += g.mixed ? 1 : 0;
-  bool mixed = waves >= 0.5 && waves < 1.5 && dump.slot == nullptr && e->cat.M <= 32 && n_mixable >= 2;
+  bool mixed = waves >= 0.5 && waves < 1.8 && dump.slot == nullptr && e->cat.M <= 32 && n_mixable >= 2;
   if (const char* v = std::getenv("CACE_MIXED")) mixed = v[0] == '1' ? (dump.slot == nullptr && e->cat.M <= 32 &&
                                                                           n_mixable >= 1)
                                                                        : false;  // A/B switch (0 / 1)
